@@ -1,0 +1,260 @@
+/*
+ * psg.h — C ABI of the B200 plan-search engine ("psg" = plan search on GPU).
+ *
+ * This is the drop-in boundary for the reference's evaluate-all-plans call
+ *
+ *     RankedPlans plansim::search(const std::vector<ExecutionPlan>& plans,
+ *                                 const ModelSpec&, const ClusterSpec&,
+ *                                 const Trace&, const ProfileStore&, Objective,
+ *                                 const std::vector<double>& frequencies,
+ *                                 const SimConfig& cfg, int jobs);
+ *   (/root/reference/proj/include/plansim/simulator.hpp:99-103,
+ *    implementation /root/reference/proj/src/simulator.cpp:242-296)
+ *
+ * and, with a one-plan / one-frequency set, of
+ *
+ *     SimulationReport plansim::simulate_plan(...)   (simulator.hpp:80-82).
+ *
+ * Everything crossing this boundary is plain C: structure-of-arrays views
+ * over caller-owned memory, sizes, and library-owned results released with
+ * psg_result_free().  No C++ or torch types appear here.  Each struct field
+ * names the reference field it flattens.
+ *
+ * Error behaviour mirrors the reference's exceptions: PSG_ERR_INFEASIBLE for
+ * InfeasibleError (empty plan list, simulator.cpp:247), PSG_ERR_DATA for
+ * DataError (missing profile table when an iteration queries it,
+ * cost.cpp:178-189 / :262-270; chunk_size < 1 in chunked mode,
+ * batching.cpp:63-64).  The message is available from psg_last_error().
+ */
+#ifndef PSG_H_
+#define PSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_ABI_VERSION 1
+
+/* Return codes (the reference CLI's exit codes, tools/plansim_main.cpp:28-31). */
+enum {
+  PSG_OK = 0,
+  PSG_ERR_USAGE = 2,      /* malformed arguments to this ABI */
+  PSG_ERR_INFEASIBLE = 3, /* plansim::InfeasibleError */
+  PSG_ERR_DATA = 4,       /* plansim::DataError */
+  PSG_ERR_CUDA = 5        /* device / driver failure (no reference analogue) */
+};
+
+/* plansim::OpKind (cost.hpp:20). */
+enum { PSG_OP_ATTENTION = 0, PSG_OP_GEMM = 1, PSG_OP_MOE_GEMM = 2 };
+/* plansim::CollectiveKind (cost.hpp:21). */
+enum {
+  PSG_COLL_ALLREDUCE = 0,
+  PSG_COLL_ALLGATHER = 1,
+  PSG_COLL_REDUCE_SCATTER = 2,
+  PSG_COLL_ALL_TO_ALL = 3,
+  PSG_COLL_P2P = 4
+};
+/* plansim::Dtype (ir.hpp:13). */
+enum { PSG_DTYPE_FP16 = 0, PSG_DTYPE_FP8 = 1, PSG_DTYPE_INT4 = 2 };
+/* plansim::Objective (simulator.hpp:84). */
+enum { PSG_OBJ_LATENCY = 0, PSG_OBJ_ENERGY = 1 };
+/* plansim::BatchMode (batching.hpp:15). */
+enum { PSG_BATCH_CONTIGUOUS = 0, PSG_BATCH_CHUNKED = 1 };
+/* plansim::TtftAnchor (simulator.hpp:71). */
+enum { PSG_ANCHOR_ARRIVAL = 0, PSG_ANCHOR_ADMISSION = 1 };
+
+/*
+ * Flattened std::vector<ExecutionPlan> (planner.hpp:92-106).  Per-plan
+ * scalars are arrays of length n_plans; the variable-length lists (cells,
+ * block_collectives, p2p_boundary_nodes) are CSR arrays whose *_begin index
+ * arrays have n_plans + 1 entries.
+ */
+typedef struct psg_plan_set {
+  int32_t n_plans;
+  const int32_t* model_dp;            /* scheme.model_dp */
+  const int32_t* num_stages;          /* scheme.num_stages */
+  const int32_t* stage_devices;       /* scheme.stage_devices */
+  const int32_t* stage_repetitions;   /* scheme.stage_repetitions */
+  const int32_t* compute_dtype;       /* compute_dtype (PSG_DTYPE_*) */
+  const int32_t* enc_rank;            /* rank of scheme.encoding under std::string operator<
+                                         (equal strings share a rank) */
+  const double* kv_bytes_per_token;   /* kv_bytes_per_token */
+  const double* kv_budget_per_replica;/* kv_budget_per_replica */
+  const double* p2p_payload_per_token;/* p2p_payload_per_token */
+  const double* shape_hidden;         /* op_shape.model_hidden */
+  const double* shape_head_dim;       /* op_shape.head_dim */
+  const double* shape_kv_elems;       /* op_shape.kv_elems_per_task_token */
+  /* scheme.cells[] (CellScheme, planner.hpp:27-41) */
+  const int32_t* cell_begin;          /* [n_plans + 1] */
+  const int32_t* cell_op;             /* CellScheme::op (PSG_OP_*) */
+  const double* cell_tasks;           /* CellScheme::query_tasks */
+  const double* cell_width;           /* CellScheme::query_width */
+  const double* cell_token_scale;     /* CellScheme::token_scale */
+  /* block_collectives[] (ResolvedCollective, planner.hpp:83-90) */
+  const int32_t* coll_begin;          /* [n_plans + 1] */
+  const int32_t* coll_kind;           /* PSG_COLL_* */
+  const int32_t* coll_devices;        /* num_devices */
+  const int32_t* coll_nodes;          /* num_nodes */
+  const int32_t* coll_groups;         /* groups_per_stage */
+  const double* coll_ppt;             /* payload_bytes_per_token */
+  const double* coll_share;           /* token_share */
+  /* p2p_boundary_nodes[] (one per stage boundary) */
+  const int32_t* p2p_begin;           /* [n_plans + 1] */
+  const int32_t* p2p_nodes;
+} psg_plan_set;
+
+/* The parts of ClusterSpec (cluster.hpp:22-46) the evaluation reads. */
+typedef struct psg_cluster {
+  int32_t total_devices;              /* ClusterSpec::total_devices() */
+  double peak_mem_bandwidth;          /* device.peak_mem_bandwidth */
+  double peak_flops[3];               /* device.peak_flops by PSG_DTYPE_*; <= 0: absent */
+  double max_frequency_ghz;           /* device.max_frequency() */
+} psg_cluster;
+
+/*
+ * Flattened, finalized ProfileStore (cost.hpp:63-129).  Compute grid t has
+ * knots[knot_begin[t] ...] laid out as ctx[n_ctx], tasks[n_tasks],
+ * width[n_width] (each strictly ascending), and values
+ * seconds/joules[value_begin[t] ...] row-major over (ctx, tasks, width).
+ * Collective curve u has payload/seconds/joules[curve_begin[u] ...][n].
+ */
+typedef struct psg_store {
+  int32_t n_compute;
+  const int32_t* c_op;
+  const int32_t* c_dtype;
+  const int64_t* c_freq_micro;        /* llround(freq_ghz * 1e6), cost.cpp:77 */
+  const int32_t* c_n_ctx;
+  const int32_t* c_n_tasks;
+  const int32_t* c_n_width;
+  const int64_t* c_knot_begin;
+  const int64_t* c_value_begin;
+  const double* c_knots;
+  const double* c_seconds;
+  const double* c_joules;
+  int32_t n_curves;
+  const int32_t* k_kind;
+  const int32_t* k_devices;
+  const int32_t* k_nodes;
+  const int32_t* k_n;
+  const int64_t* k_begin;
+  const double* k_payload;
+  const double* k_seconds;
+  const double* k_joules;
+} psg_store;
+
+/* plansim::Trace (traces.hpp:14-31): requests in trace order. */
+typedef struct psg_trace {
+  int64_t n;
+  const int64_t* id;
+  const int64_t* context_len;
+  const int64_t* gen_len;
+  const double* arrival;
+} psg_trace;
+
+/* SimConfig (simulator.hpp:73-78) + the other search() arguments. */
+typedef struct psg_config {
+  int32_t objective;                  /* PSG_OBJ_* */
+  int32_t batch_mode;                 /* PSG_BATCH_* (BatchPolicy::mode) */
+  int64_t chunk_size;                 /* BatchPolicy::chunk_size */
+  int64_t max_batch_size;             /* BatchPolicy::max_batch_size, 0 = unlimited */
+  int32_t ttft_anchor;                /* PSG_ANCHOR_* */
+  int32_t n_freqs;                    /* frequencies; 0 => {max_frequency_ghz} */
+  const double* freqs;
+  int32_t detail;                     /* 1: return per-request metrics + rejected ids
+                                         (drop-in); 0: summaries only */
+  int32_t rank;                       /* 1: sort entries (search); 0: entry order */
+  int32_t n_entry_subset;             /* >0: simulate only these entry indices (sharding) */
+  const int32_t* entry_subset;
+} psg_config;
+
+/* plansim::RequestMetrics (simulator.hpp:44-50); identical layout (40 B). */
+typedef struct psg_request_metrics {
+  int64_t id;
+  double ttft;
+  double tpot;
+  double e2e;
+  int64_t gen_len;
+} psg_request_metrics;
+
+/* One SearchEntry + SimulationReport scalars (simulator.hpp:52-69, :86-90). */
+typedef struct psg_entry {
+  int64_t entry_index;                /* i: plan i / F, freq i % F (simulator.cpp:255-258) */
+  int64_t plan_index;
+  double freq_ghz;
+  double e2e_latency;
+  double total_energy;
+  double p95_latency;
+  double mean_ttft;
+  double mean_tpot;
+  double mfu;
+  double mbu;
+  int64_t num_completed;
+  int64_t num_rejected;
+  int64_t num_iterations;
+  int64_t max_batch_observed;
+  /* additive outputs the reference does not compute (nearest-rank rule of
+     simulator.cpp:223-225 applied at 0.50 / 0.99) */
+  double p50_ttft, p99_ttft, p50_tpot, p99_tpot;
+  int64_t per_request_offset;         /* into psg_result.per_request */
+  int64_t rejected_offset;            /* into psg_result.rejected_ids */
+} psg_entry;
+
+/* Ranking record exchanged between ranks for the multi-GPU merge. */
+typedef struct psg_rank_key {
+  int64_t num_rejected;
+  double objective_metric;
+  double other_metric;
+  int32_t enc_rank;
+  int32_t pad_;
+  double freq_ghz;
+  int64_t entry_index;
+} psg_rank_key;
+
+typedef struct psg_result {
+  int64_t n_entries;
+  psg_entry* entries;                 /* ranked best-first when config.rank, else entry order */
+  int64_t n_per_request;
+  psg_request_metrics* per_request;   /* per entry sorted by id (simulator.cpp:205-206) */
+  int64_t n_rejected;
+  int64_t* rejected_ids;              /* per entry sorted (simulator.cpp:207) */
+  int32_t n_compute;
+  uint8_t* compute_clamp;             /* per store compute grid: bit 2*axis + (above) */
+  int32_t n_curves;
+  uint8_t* curve_clamp;               /* per collective curve: bit 0 below, bit 1 above */
+  /* instrumentation */
+  int64_t gpu_launches;               /* kernels launched by this call */
+  int64_t total_iterations;           /* sum of num_iterations over entries */
+  double ms_total;                    /* host wall time of the call */
+  double ms_h2d, ms_sim, ms_reduce, ms_d2h;  /* CUDA-event times of the phases */
+} psg_result;
+
+typedef struct psg_context psg_context;
+
+const char* psg_version(void);
+
+/* One context per device; a context is not thread-shared. */
+int psg_context_create(int device, psg_context** out);
+void psg_context_destroy(psg_context* ctx);
+const char* psg_last_error(const psg_context* ctx);
+
+/* Evaluate-all-plans: plansim::search semantics (see header comment). */
+int psg_search(psg_context* ctx, const psg_plan_set* plans,
+               const psg_cluster* cluster, const psg_store* store,
+               const psg_trace* trace, const psg_config* config,
+               psg_result** out);
+
+/* Device ranking of gathered keys (multi-GPU merge): order[k] = index into
+   keys of the k-th best entry under the comparator of simulator.cpp:283-294. */
+int psg_rank_keys(psg_context* ctx, const psg_rank_key* keys, int64_t n,
+                  int64_t* order);
+
+void psg_result_free(psg_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSG_H_ */

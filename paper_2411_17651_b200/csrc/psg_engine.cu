@@ -1,0 +1,689 @@
+// psg_engine.cu — host orchestration behind the C ABI (include/psg.h).
+//
+// One psg_search() call = the reference's search() (simulator.cpp:242-296):
+//   1. resolve every (plan, frequency) entry's profile tables once on the
+//      host (the reference does a std::map lookup per query, cost.cpp:178-189
+//      / :262-270), canonicalize the trace (id-order slots, replica order);
+//   2. one H2D of a packed, 16-byte-aligned input image from pinned memory;
+//   3. sim_kernel over all (plan, freq, replica) units, LPT-ordered;
+//   4. entry_reduce_kernel + offsets + rank_kernel;
+//   5. one D2H of entry records, then compact_kernel + one D2H of the dense
+//      per-request / rejected arrays (sorted by id, simulator.cpp:205-207).
+// Device and pinned buffers are cached in the context and only grow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "psg.h"
+#include "psg_device.cuh"
+#include "psg_reduce.cuh"
+
+using namespace psg;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n, 1024);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n + n / 4, 4096);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Builds the packed input image: arrays appended at 16-byte alignment.
+struct Packer {
+  std::vector<std::tuple<size_t, const void*, size_t>> parts;  // offset, src, bytes
+  size_t size = 0;
+  template <typename T>
+  size_t add(const T* src, size_t count) {
+    size = (size + 15) & ~size_t(15);
+    const size_t off = size;
+    const size_t bytes = sizeof(T) * count;
+    parts.emplace_back(off, src, bytes);
+    size += bytes;
+    return off;
+  }
+  void write(unsigned char* dst) const {
+    for (const auto& [off, src, bytes] : parts)
+      if (bytes) std::memcpy(dst + off, src, bytes);
+  }
+};
+
+const char* op_name(int op) {
+  switch (op) {
+    case PSG_OP_ATTENTION: return "attention";
+    case PSG_OP_GEMM: return "gemm";
+    case PSG_OP_MOE_GEMM: return "moe_gemm";
+  }
+  return "?";
+}
+const char* coll_name(int k) {
+  switch (k) {
+    case PSG_COLL_ALLREDUCE: return "allreduce";
+    case PSG_COLL_ALLGATHER: return "allgather";
+    case PSG_COLL_REDUCE_SCATTER: return "reduce_scatter";
+    case PSG_COLL_ALL_TO_ALL: return "all_to_all";
+    case PSG_COLL_P2P: return "p2p";
+  }
+  return "?";
+}
+const char* dtype_name(int d) {
+  switch (d) {
+    case PSG_DTYPE_FP16: return "fp16";
+    case PSG_DTYPE_FP8: return "fp8";
+    case PSG_DTYPE_INT4: return "int4";
+  }
+  return "?";
+}
+
+}  // namespace
+
+struct psg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  std::string err;
+  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj;
+  HostBuf h_in, h_out, h_pr, h_rj;
+  // storage for results handed out (valid until the next call)
+  std::vector<psg_entry> entries;
+  std::vector<uint8_t> compute_clamp, curve_clamp;
+};
+
+namespace {
+
+int fail(psg_context* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define PSG_CUDA(call)                                                           \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(ctx, PSG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* psg_version(void) { return "psg-b200 1 (sm_100a)"; }
+
+int psg_context_create(int device, psg_context** out) {
+  if (!out) return PSG_ERR_USAGE;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return PSG_ERR_CUDA;
+  if (device < 0 || device >= count) return PSG_ERR_USAGE;
+  if (cudaSetDevice(device) != cudaSuccess) return PSG_ERR_CUDA;
+  auto* ctx = new psg_context();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return PSG_ERR_CUDA;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return PSG_OK;
+}
+
+void psg_context_destroy(psg_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
+                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj})
+    b->release();
+  for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj}) b->release();
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* psg_last_error(const psg_context* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+void psg_result_free(psg_result* r) { delete r; }
+
+int psg_rank_keys(psg_context* ctx, const psg_rank_key* keys, int64_t n, int64_t* order) {
+  if (!ctx || (n > 0 && (!keys || !order))) return PSG_ERR_USAGE;
+  if (n == 0) return PSG_OK;
+  PSG_CUDA(cudaSetDevice(ctx->device));
+  const size_t kb = sizeof(psg_rank_key) * size_t(n), ob = sizeof(int64_t) * size_t(n);
+  PSG_CUDA(ctx->d_work.ensure(kb + ob + 64));
+  PSG_CUDA(ctx->h_out.ensure(kb + ob));
+  auto* dk = static_cast<psg_rank_key*>(ctx->d_work.p);
+  auto* dord = reinterpret_cast<int64_t*>(static_cast<unsigned char*>(ctx->d_work.p) + ((kb + 15) & ~size_t(15)));
+  std::memcpy(ctx->h_out.p, keys, kb);
+  PSG_CUDA(cudaMemcpyAsync(dk, ctx->h_out.p, kb, cudaMemcpyHostToDevice, ctx->stream));
+  rank_kernel<<<unsigned((n + 255) / 256), 256, 0, ctx->stream>>>(dk, n, dord);
+  PSG_CUDA(cudaGetLastError());
+  PSG_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(ctx->h_out.p) + kb, dord, ob,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(order, static_cast<unsigned char*>(ctx->h_out.p) + kb, ob);
+  return PSG_OK;
+}
+
+int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
+               const psg_store* S, const psg_trace* T, const psg_config* cfg,
+               psg_result** out) {
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  if (!ctx || !P || !cl || !S || !T || !cfg || !out) return PSG_ERR_USAGE;
+  *out = nullptr;
+  ctx->err.clear();
+  if (P->n_plans <= 0) return fail(ctx, PSG_ERR_INFEASIBLE, "search: no feasible plan");
+  PSG_CUDA(cudaSetDevice(ctx->device));
+
+  // ---- frequencies and entries (simulator.cpp:248-258) ----
+  std::vector<double> freqs(cfg->freqs, cfg->freqs + std::max(0, cfg->n_freqs));
+  if (freqs.empty()) freqs.push_back(cl->max_frequency_ghz);
+  const int F = int(freqs.size());
+  const int64_t n_total_entries = int64_t(P->n_plans) * F;
+  std::vector<int64_t> ent;  // local entry -> global entry index
+  if (cfg->n_entry_subset > 0) {
+    for (int i = 0; i < cfg->n_entry_subset; ++i) {
+      const int64_t g = cfg->entry_subset[i];
+      if (g < 0 || g >= n_total_entries) return fail(ctx, PSG_ERR_USAGE, "entry_subset out of range");
+      ent.push_back(g);
+    }
+  } else {
+    ent.resize(size_t(n_total_entries));
+    std::iota(ent.begin(), ent.end(), 0);
+  }
+  const int E = int(ent.size());
+
+  // ---- validate plans ----
+  const int np = P->n_plans;
+  const int n_cells = P->cell_begin[np], n_colls = P->coll_begin[np], n_p2p = P->p2p_begin[np];
+  for (int p = 0; p < np; ++p) {
+    const int C = P->cell_begin[p + 1] - P->cell_begin[p];
+    const int K = P->coll_begin[p + 1] - P->coll_begin[p];
+    const int NB = P->p2p_begin[p + 1] - P->p2p_begin[p];
+    if (C < 0 || K < 0 || NB < 0 || C > kMaxCells || C + K + NB > kMaxClampSlots)
+      return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": unsupported cell/collective count");
+    if (P->model_dp[p] < 1 || P->num_stages[p] < 1)
+      return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": bad degrees");
+    if (NB != P->num_stages[p] - 1)
+      return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": p2p boundaries != stages-1");
+  }
+
+  // ---- resolve tables (ProfileStore keys, cost.hpp:105-116) ----
+  std::map<std::tuple<int, int, long long>, int> cmap;
+  for (int t = 0; t < S->n_compute; ++t) {
+    if (S->c_n_ctx[t] < 1 || S->c_n_tasks[t] < 1 || S->c_n_width[t] < 1)
+      return fail(ctx, PSG_ERR_DATA, "profile: empty compute grid");
+    cmap[{S->c_op[t], S->c_dtype[t], (long long)S->c_freq_micro[t]}] = t;
+  }
+  std::map<std::tuple<int, int, int>, int> kmap;
+  for (int u = 0; u < S->n_curves; ++u) {
+    if (S->k_n[u] < 1) return fail(ctx, PSG_ERR_DATA, "profile: empty collective curve");
+    kmap[{S->k_kind[u], S->k_devices[u], S->k_nodes[u]}] = u;
+  }
+  std::vector<int32_t> cell_tab(size_t(F) * n_cells, -1), coll_tab(n_colls, -1), p2p_tab(n_p2p, -1);
+  for (int f = 0; f < F; ++f) {
+    const long long fk = llround(freqs[f] * 1e6);
+    for (int p = 0; p < np; ++p)
+      for (int c = P->cell_begin[p]; c < P->cell_begin[p + 1]; ++c) {
+        auto it = cmap.find({P->cell_op[c], P->compute_dtype[p], fk});
+        cell_tab[size_t(f) * n_cells + c] = it == cmap.end() ? -1 : it->second;
+      }
+  }
+  for (int k = 0; k < n_colls; ++k) {
+    auto it = kmap.find({P->coll_kind[k], P->coll_devices[k], P->coll_nodes[k]});
+    coll_tab[k] = it == kmap.end() ? -1 : it->second;
+  }
+  for (int b = 0; b < n_p2p; ++b) {
+    auto it = kmap.find({int(PSG_COLL_P2P), 2, P->p2p_nodes[b]});
+    p2p_tab[b] = it == kmap.end() ? -1 : it->second;
+  }
+  std::vector<int32_t> entry_missing(E, 0);
+  std::vector<std::string> missing_msg(E);
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F), f = int(ent[e] % F);
+    for (int c = P->cell_begin[p]; c < P->cell_begin[p + 1] && !entry_missing[e]; ++c)
+      if (cell_tab[size_t(f) * n_cells + c] < 0) {
+        entry_missing[e] = 1;
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "profile: no compute table for op=%s dtype=%s freq=%g GHz",
+                      op_name(P->cell_op[c]), dtype_name(P->compute_dtype[p]), freqs[f]);
+        missing_msg[e] = buf;
+      }
+    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1] && !entry_missing[e]; ++k)
+      if (coll_tab[k] < 0) {
+        entry_missing[e] = 1;
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "profile: no collective table for op=%s devices=%d nodes=%d",
+                      coll_name(P->coll_kind[k]), P->coll_devices[k], P->coll_nodes[k]);
+        missing_msg[e] = buf;
+      }
+    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1] && !entry_missing[e]; ++b)
+      if (p2p_tab[b] < 0) {
+        entry_missing[e] = 1;
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "profile: no collective table for op=p2p devices=2 nodes=%d",
+                      P->p2p_nodes[b]);
+        missing_msg[e] = buf;
+      }
+  }
+
+  // ---- trace canonicalization ----
+  const int64_t N = T->n;
+  if (N < 0 || N >= INT32_MAX) return fail(ctx, PSG_ERR_USAGE, "trace too large");
+  int64_t tok_total = 0;
+  bool sorted = true;
+  for (int64_t i = 0; i < N; ++i) {
+    if (T->context_len[i] < 0 || T->context_len[i] >= INT32_MAX || T->gen_len[i] >= INT32_MAX)
+      return fail(ctx, PSG_ERR_USAGE, "trace lengths outside the supported int32 range");
+    tok_total += T->context_len[i] + std::max<int64_t>(T->gen_len[i], 1);
+    if (i && T->arrival[i] < T->arrival[i - 1]) sorted = false;
+  }
+  // Exact ledger: the reference recomputes sum(double(ctx+gen)*kv); with an
+  // integral kv every partial sum below 2^53 is exact, so token counts times
+  // kv reproduce it bit for bit.
+  for (int p = 0; p < np; ++p) {
+    const double kv = P->kv_bytes_per_token[p];
+    if (!(kv >= 0) || kv != std::floor(kv) || double(tok_total) * kv >= 9007199254740992.0)
+      return fail(ctx, PSG_ERR_USAGE,
+                  "kv_bytes_per_token must be a non-negative integer with an exactly "
+                  "representable ledger");
+  }
+  std::vector<int32_t> slot(N), slot_order(N);
+  std::iota(slot_order.begin(), slot_order.end(), 0);
+  std::stable_sort(slot_order.begin(), slot_order.end(),
+                   [&](int32_t a, int32_t b) { return T->id[a] < T->id[b]; });
+  std::vector<int64_t> slot_id(N), slot_gen(N);
+  for (int64_t s = 0; s < N; ++s) {
+    slot[slot_order[s]] = int32_t(s);
+    slot_id[s] = T->id[slot_order[s]];
+    slot_gen[s] = T->gen_len[slot_order[s]];
+  }
+
+  // ---- units: (entry, replica), longest-first ----
+  std::vector<Unit> units;
+  std::vector<int32_t> seq;
+  std::map<int, int64_t> seq_base_of;  // replicas -> base (unsorted traces only)
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F);
+    const int R = P->model_dp[p];
+    if (!sorted && !seq_base_of.count(R)) {
+      // split round-robin in trace order, then stable-sort each replica by
+      // arrival (BatchState's constructor, batching.cpp:16-17)
+      seq_base_of[R] = int64_t(seq.size());
+      for (int r = 0; r < R; ++r) {
+        std::vector<int32_t> idx;
+        for (int64_t i = r; i < N; i += R) idx.push_back(int32_t(i));
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int32_t a, int32_t b) { return T->arrival[a] < T->arrival[b]; });
+        seq.insert(seq.end(), idx.begin(), idx.end());
+      }
+    }
+    int64_t off = 0;
+    for (int r = 0; r < R; ++r) {
+      Unit u;
+      u.entry = e;
+      u.plan = p;
+      u.fslot = int(ent[e] % F);
+      u.replica = r;
+      u.replicas = R;
+      u.n_req = int32_t(N > r ? (N - r + R - 1) / R : 0);
+      u.seq_base = sorted ? 0 : seq_base_of[R] + off;
+      off += u.n_req;
+      u.scratch = 0;
+      units.push_back(u);
+    }
+  }
+  std::vector<int32_t> entry_unit_begin(E + 1, 0), entry_units(units.size());
+  {
+    std::vector<int32_t> perm(units.size());
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int32_t a, int32_t b) { return units[a].n_req > units[b].n_req; });
+    std::vector<Unit> sorted_units(units.size());
+    std::vector<int32_t> pos_of(units.size());
+    int64_t scratch = 0;
+    for (size_t k = 0; k < perm.size(); ++k) {
+      sorted_units[k] = units[perm[k]];
+      sorted_units[k].scratch = scratch;
+      scratch += sorted_units[k].n_req;
+      pos_of[perm[k]] = int32_t(k);
+    }
+    // units were generated entry-major, replica order
+    for (size_t k = 0; k < units.size(); ++k) {
+      entry_units[k] = pos_of[k];
+      entry_unit_begin[units[k].entry + 1]++;
+    }
+    for (int e = 0; e < E; ++e) entry_unit_begin[e + 1] += entry_unit_begin[e];
+    units.swap(sorted_units);
+  }
+  int64_t scratch_total = 0;
+  for (const auto& u : units) scratch_total += u.n_req;
+  const int n_units = int(units.size());
+
+  std::vector<double> entry_peak(E), entry_freq(E);
+  std::vector<int32_t> entry_enc(E);
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F);
+    const int dt = P->compute_dtype[p];
+    const double pf = (dt >= 0 && dt < 3) ? cl->peak_flops[dt] : 0.0;
+    entry_peak[e] = pf > 0 ? pf * double(cl->total_devices) : 0.0;
+    entry_freq[e] = freqs[ent[e] % F];
+    entry_enc[e] = P->enc_rank[p];
+  }
+
+  // ---- pack inputs ----
+  Packer pk;
+  const size_t o_model_dp = pk.add(P->model_dp, np), o_stages = pk.add(P->num_stages, np),
+               o_sdev = pk.add(P->stage_devices, np), o_reps = pk.add(P->stage_repetitions, np),
+               o_dtype = pk.add(P->compute_dtype, np), o_enc = pk.add(P->enc_rank, np),
+               o_kv = pk.add(P->kv_bytes_per_token, np), o_budget = pk.add(P->kv_budget_per_replica, np),
+               o_p2pppt = pk.add(P->p2p_payload_per_token, np), o_hid = pk.add(P->shape_hidden, np),
+               o_head = pk.add(P->shape_head_dim, np), o_kve = pk.add(P->shape_kv_elems, np),
+               o_cb = pk.add(P->cell_begin, np + 1), o_cop = pk.add(P->cell_op, n_cells),
+               o_ct = pk.add(P->cell_tasks, n_cells), o_cw = pk.add(P->cell_width, n_cells),
+               o_cs = pk.add(P->cell_token_scale, n_cells), o_kb = pk.add(P->coll_begin, np + 1),
+               o_kk = pk.add(P->coll_kind, n_colls), o_kd = pk.add(P->coll_devices, n_colls),
+               o_kn = pk.add(P->coll_nodes, n_colls), o_kg = pk.add(P->coll_groups, n_colls),
+               o_kp = pk.add(P->coll_ppt, n_colls), o_ksh = pk.add(P->coll_share, n_colls),
+               o_pb = pk.add(P->p2p_begin, np + 1), o_pn = pk.add(P->p2p_nodes, n_p2p);
+  int64_t n_knots = 0, n_vals = 0, n_kpts = 0;
+  for (int t = 0; t < S->n_compute; ++t) {
+    n_knots = std::max<int64_t>(n_knots, S->c_knot_begin[t] + S->c_n_ctx[t] + S->c_n_tasks[t] + S->c_n_width[t]);
+    n_vals = std::max<int64_t>(n_vals, S->c_value_begin[t] + int64_t(S->c_n_ctx[t]) * S->c_n_tasks[t] * S->c_n_width[t]);
+  }
+  for (int u = 0; u < S->n_curves; ++u) n_kpts = std::max<int64_t>(n_kpts, S->k_begin[u] + S->k_n[u]);
+  const size_t o_snc = pk.add(S->c_n_ctx, S->n_compute), o_snt = pk.add(S->c_n_tasks, S->n_compute),
+               o_snw = pk.add(S->c_n_width, S->n_compute), o_skb = pk.add(S->c_knot_begin, S->n_compute),
+               o_svb = pk.add(S->c_value_begin, S->n_compute), o_sk = pk.add(S->c_knots, n_knots),
+               o_ss = pk.add(S->c_seconds, n_vals), o_sj = pk.add(S->c_joules, n_vals),
+               o_kn2 = pk.add(S->k_n, S->n_curves), o_kbeg = pk.add(S->k_begin, S->n_curves),
+               o_kpay = pk.add(S->k_payload, n_kpts), o_ksec = pk.add(S->k_seconds, n_kpts),
+               o_kjou = pk.add(S->k_joules, n_kpts);
+  const size_t o_tctx = pk.add(T->context_len, N), o_tgen = pk.add(T->gen_len, N),
+               o_tarr = pk.add(T->arrival, N), o_tslot = pk.add(slot.data(), N),
+               o_tseq = pk.add(seq.data(), seq.size()), o_sid = pk.add(slot_id.data(), N),
+               o_sgen = pk.add(slot_gen.data(), N);
+  const size_t o_freqs = pk.add(freqs.data(), freqs.size()),
+               o_celltab = pk.add(cell_tab.data(), cell_tab.size()),
+               o_colltab = pk.add(coll_tab.data(), coll_tab.size()),
+               o_p2ptab = pk.add(p2p_tab.data(), p2p_tab.size()),
+               o_emiss = pk.add(entry_missing.data(), E),
+               o_units = pk.add(units.data(), units.size()),
+               o_eub = pk.add(entry_unit_begin.data(), E + 1),
+               o_eu = pk.add(entry_units.data(), entry_units.size()),
+               o_epeak = pk.add(entry_peak.data(), E), o_eenc = pk.add(entry_enc.data(), E),
+               o_efreq = pk.add(entry_freq.data(), E), o_eglob = pk.add(ent.data(), E);
+  const size_t in_bytes = pk.size;
+
+  // ---- device buffers ----
+  const size_t slots = size_t(E) * size_t(N);
+  PSG_CUDA(ctx->d_in.ensure(in_bytes));
+  PSG_CUDA(ctx->h_in.ensure(in_bytes));
+  PSG_CUDA(ctx->d_slot_f64.ensure(std::max<size_t>(slots, 1) * 3 * sizeof(double)));
+  PSG_CUDA(ctx->d_slot_u8.ensure(std::max<size_t>(slots, 1)));
+  PSG_CUDA(ctx->d_scratch_i32.ensure(std::max<int64_t>(scratch_total, 1) * 6 * sizeof(int32_t)));
+  PSG_CUDA(ctx->d_scratch_f64.ensure(std::max<int64_t>(scratch_total, 1) * 3 * sizeof(double)));
+  // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
+  Packer wk;  // offsets only
+  const size_t w_uout = wk.add<UnitOut>(nullptr, n_units), w_eout = wk.add<EntryOut>(nullptr, E),
+               w_keys = wk.add<psg_rank_key>(nullptr, E), w_order = wk.add<int64_t>(nullptr, E),
+               w_proff = wk.add<int64_t>(nullptr, E), w_rjoff = wk.add<int64_t>(nullptr, E),
+               w_tot = wk.add<int64_t>(nullptr, 2), w_cc = wk.add<uint32_t>(nullptr, S->n_compute),
+               w_kc = wk.add<uint32_t>(nullptr, S->n_curves);
+  PSG_CUDA(ctx->d_work.ensure(wk.size + 64));
+  PSG_CUDA(ctx->h_out.ensure(wk.size + 64));
+
+  unsigned char* hin = static_cast<unsigned char*>(ctx->h_in.p);
+  pk.write(hin);
+  unsigned char* din = static_cast<unsigned char*>(ctx->d_in.p);
+  unsigned char* dw = static_cast<unsigned char*>(ctx->d_work.p);
+  auto D = [&](size_t off) { return static_cast<void*>(din + off); };
+  auto W = [&](size_t off) { return static_cast<void*>(dw + off); };
+
+  SimParams sp{};
+  sp.P = DPlans{np,
+                (const int32_t*)D(o_model_dp), (const int32_t*)D(o_stages), (const int32_t*)D(o_sdev),
+                (const int32_t*)D(o_reps), (const int32_t*)D(o_dtype), (const int32_t*)D(o_enc),
+                (const double*)D(o_kv), (const double*)D(o_budget), (const double*)D(o_p2pppt),
+                (const double*)D(o_hid), (const double*)D(o_head), (const double*)D(o_kve),
+                (const int32_t*)D(o_cb), (const int32_t*)D(o_cop), (const double*)D(o_ct),
+                (const double*)D(o_cw), (const double*)D(o_cs), (const int32_t*)D(o_kb),
+                (const int32_t*)D(o_kk), (const int32_t*)D(o_kd), (const int32_t*)D(o_kn),
+                (const int32_t*)D(o_kg), (const double*)D(o_kp), (const double*)D(o_ksh),
+                (const int32_t*)D(o_pb), (const int32_t*)D(o_pn)};
+  sp.S = DStore{(const int32_t*)D(o_snc), (const int32_t*)D(o_snt), (const int32_t*)D(o_snw),
+                (const int64_t*)D(o_skb), (const int64_t*)D(o_svb), (const double*)D(o_sk),
+                (const double*)D(o_ss), (const double*)D(o_sj), (const int32_t*)D(o_kn2),
+                (const int64_t*)D(o_kbeg), (const double*)D(o_kpay), (const double*)D(o_ksec),
+                (const double*)D(o_kjou)};
+  sp.T = DTrace{N, (const int64_t*)D(o_tctx), (const int64_t*)D(o_tgen), (const double*)D(o_tarr),
+                (const int32_t*)D(o_tslot), sorted ? nullptr : (const int32_t*)D(o_tseq)};
+  sp.freqs = (const double*)D(o_freqs);
+  sp.cell_tab = (const int32_t*)D(o_celltab);
+  sp.coll_tab = (const int32_t*)D(o_colltab);
+  sp.p2p_tab = (const int32_t*)D(o_p2ptab);
+  sp.entry_missing = (const int32_t*)D(o_emiss);
+  sp.n_cells_total = n_cells;
+  sp.units = (const Unit*)D(o_units);
+  sp.n_units = n_units;
+  sp.batch_mode = cfg->batch_mode;
+  sp.chunk_size = cfg->chunk_size;
+  sp.max_batch_size = cfg->max_batch_size;
+  sp.anchor = cfg->ttft_anchor;
+  sp.smem_cap = 256;
+  sp.memo_cap = 256;
+  sp.n_slots = N;
+  sp.uout = (UnitOut*)W(w_uout);
+  double* slot_f = static_cast<double*>(ctx->d_slot_f64.p);
+  sp.slot_ttft = slot_f;
+  sp.slot_tpot = slot_f + slots;
+  sp.slot_e2e = slot_f + 2 * slots;
+  sp.slot_status = static_cast<uint8_t*>(ctx->d_slot_u8.p);
+  sp.clamp_compute = (uint32_t*)W(w_cc);
+  sp.clamp_curve = (uint32_t*)W(w_kc);
+  sp.g_i32 = static_cast<int32_t*>(ctx->d_scratch_i32.p);
+  sp.g_f64 = static_cast<double*>(ctx->d_scratch_f64.p);
+
+  ReduceParams rp{};
+  rp.n_slots = N;
+  rp.slot_status = sp.slot_status;
+  rp.slot_ttft = sp.slot_ttft;
+  rp.slot_tpot = sp.slot_tpot;
+  rp.slot_e2e = sp.slot_e2e;
+  rp.slot_gen = (const int64_t*)D(o_sgen);
+  rp.slot_id = (const int64_t*)D(o_sid);
+  rp.uout = sp.uout;
+  rp.entry_unit_begin = (const int32_t*)D(o_eub);
+  rp.entry_units = (const int32_t*)D(o_eu);
+  rp.entry_peak = (const double*)D(o_epeak);
+  rp.entry_enc_rank = (const int32_t*)D(o_eenc);
+  rp.entry_freq = (const double*)D(o_efreq);
+  rp.entry_global = (const int64_t*)D(o_eglob);
+  rp.mem_bw = cl->peak_mem_bandwidth;
+  rp.total_devices = cl->total_devices;
+  rp.objective = cfg->objective;
+  rp.extras = 1;
+  rp.eout = (EntryOut*)W(w_eout);
+  rp.keys = (psg_rank_key*)W(w_keys);
+
+  cudaStream_t st = ctx->stream;
+  int64_t launches = 0;
+  PSG_CUDA(cudaEventRecord(ctx->ev[0], st));
+  PSG_CUDA(cudaMemcpyAsync(din, hin, in_bytes, cudaMemcpyHostToDevice, st));
+  PSG_CUDA(cudaMemsetAsync(sp.slot_status, 0, std::max<size_t>(slots, 1), st));
+  PSG_CUDA(cudaMemsetAsync(W(w_cc), 0, wk.size - w_cc, st));
+  PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
+  const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap);
+  PSG_CUDA(cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (n_units > 0) {
+    sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
+    ++launches;
+    PSG_CUDA(cudaGetLastError());
+  }
+  PSG_CUDA(cudaEventRecord(ctx->ev[2], st));
+  entry_reduce_kernel<<<E, 256, 0, st>>>(rp);
+  offsets_kernel<<<1, 32, 0, st>>>(rp.eout, E, (int64_t*)W(w_proff), (int64_t*)W(w_rjoff),
+                                   (int64_t*)W(w_tot));
+  launches += 2;
+  if (cfg->rank) {
+    rank_kernel<<<unsigned((E + 255) / 256), 256, 0, st>>>(rp.keys, E, (int64_t*)W(w_order));
+    ++launches;
+  }
+  PSG_CUDA(cudaGetLastError());
+  PSG_CUDA(cudaEventRecord(ctx->ev[3], st));
+  // everything from uout onwards is small: one D2H
+  PSG_CUDA(cudaMemcpyAsync(ctx->h_out.p, dw, wk.size, cudaMemcpyDeviceToHost, st));
+  PSG_CUDA(cudaStreamSynchronize(st));
+  const unsigned char* ho = static_cast<const unsigned char*>(ctx->h_out.p);
+  auto H = [&](size_t off) { return ho + off; };
+  const auto* eo = reinterpret_cast<const EntryOut*>(H(w_eout));
+  const auto* order = reinterpret_cast<const int64_t*>(H(w_order));
+  const auto* tot = reinterpret_cast<const int64_t*>(H(w_tot));
+  const auto* proff = reinterpret_cast<const int64_t*>(H(w_proff));
+  const auto* rjoff = reinterpret_cast<const int64_t*>(H(w_rjoff));
+
+  // ---- errors: the lowest global entry index that failed (jobs=1 order) ----
+  {
+    int64_t worst = INT64_MAX;
+    int we = -1;
+    for (int e = 0; e < E; ++e)
+      if (eo[e].err && ent[e] < worst) {
+        worst = ent[e];
+        we = e;
+      }
+    if (we >= 0) {
+      const int code = eo[we].err;
+      if (code == 1) return fail(ctx, PSG_ERR_DATA, "chunked prefill requires chunk_size >= 1");
+      if (code == 2) return fail(ctx, PSG_ERR_DATA, missing_msg[we]);
+      const int p = int(ent[we] / F);
+      return fail(ctx, PSG_ERR_DATA, std::string("device has no peak_flops entry for dtype ") +
+                                         dtype_name(P->compute_dtype[p]));
+    }
+  }
+
+  // ---- per-request arrays ----
+  const int64_t n_pr = cfg->detail ? tot[0] : 0, n_rj = cfg->detail ? tot[1] : 0;
+  if (cfg->detail) {
+    PSG_CUDA(ctx->d_pr.ensure(std::max<int64_t>(n_pr, 1) * sizeof(psg_request_metrics)));
+    PSG_CUDA(ctx->d_rj.ensure(std::max<int64_t>(n_rj, 1) * sizeof(int64_t)));
+    PSG_CUDA(ctx->h_pr.ensure(std::max<int64_t>(n_pr, 1) * sizeof(psg_request_metrics)));
+    PSG_CUDA(ctx->h_rj.ensure(std::max<int64_t>(n_rj, 1) * sizeof(int64_t)));
+    compact_kernel<<<E, 256, 0, st>>>(rp, (const int64_t*)W(w_proff), (const int64_t*)W(w_rjoff),
+                                      static_cast<psg_request_metrics*>(ctx->d_pr.p),
+                                      static_cast<int64_t*>(ctx->d_rj.p));
+    ++launches;
+    PSG_CUDA(cudaGetLastError());
+    if (n_pr)
+      PSG_CUDA(cudaMemcpyAsync(ctx->h_pr.p, ctx->d_pr.p, n_pr * sizeof(psg_request_metrics),
+                               cudaMemcpyDeviceToHost, st));
+    if (n_rj)
+      PSG_CUDA(cudaMemcpyAsync(ctx->h_rj.p, ctx->d_rj.p, n_rj * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+  }
+  PSG_CUDA(cudaEventRecord(ctx->ev[4], st));
+  PSG_CUDA(cudaStreamSynchronize(st));
+
+  // ---- assemble result ----
+  ctx->entries.resize(E);
+  for (int k = 0; k < E; ++k) {
+    const int e = cfg->rank ? int(order[k]) : k;
+    const EntryOut& o = eo[e];
+    psg_entry& r = ctx->entries[k];
+    r.entry_index = ent[e];
+    r.plan_index = ent[e] / F;
+    r.freq_ghz = freqs[ent[e] % F];
+    r.e2e_latency = o.e2e;
+    r.total_energy = o.energy;
+    r.p95_latency = o.p95;
+    r.mean_ttft = o.mean_ttft;
+    r.mean_tpot = o.mean_tpot;
+    r.mfu = o.mfu;
+    r.mbu = o.mbu;
+    r.num_completed = o.completed;
+    r.num_rejected = o.rejected;
+    r.num_iterations = o.iterations;
+    r.max_batch_observed = o.max_batch;
+    r.p50_ttft = o.p50_ttft;
+    r.p99_ttft = o.p99_ttft;
+    r.p50_tpot = o.p50_tpot;
+    r.p99_tpot = o.p99_tpot;
+    r.per_request_offset = cfg->detail ? proff[e] : 0;
+    r.rejected_offset = cfg->detail ? rjoff[e] : 0;
+  }
+  const auto* cc = reinterpret_cast<const uint32_t*>(H(w_cc));
+  const auto* kc = reinterpret_cast<const uint32_t*>(H(w_kc));
+  ctx->compute_clamp.assign(cc, cc + S->n_compute);
+  ctx->curve_clamp.assign(kc, kc + S->n_curves);
+
+  auto* res = new psg_result();
+  res->n_entries = E;
+  res->entries = ctx->entries.data();
+  res->n_per_request = n_pr;
+  res->per_request = static_cast<psg_request_metrics*>(ctx->h_pr.p);
+  res->n_rejected = n_rj;
+  res->rejected_ids = static_cast<int64_t*>(ctx->h_rj.p);
+  res->n_compute = S->n_compute;
+  res->compute_clamp = ctx->compute_clamp.data();
+  res->n_curves = S->n_curves;
+  res->curve_clamp = ctx->curve_clamp.data();
+  res->gpu_launches = launches;
+  int64_t iters = 0;
+  for (int e = 0; e < E; ++e) iters += eo[e].iterations;
+  res->total_iterations = iters;
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  res->ms_h2d = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+  res->ms_sim = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  res->ms_reduce = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
+  res->ms_d2h = ms;
+  res->ms_total = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+  *out = res;
+  return PSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,280 @@
+// psg_reduce.cu — per-entry metric reduction, output compaction and ranking.
+//
+//  entry_reduce_kernel  simulate_plan's reduction (simulator.cpp:196-238):
+//                       e2e = max over replicas, energy summed in replica
+//                       order, mean TTFT/TPOT summed in ascending-id order
+//                       (one serial FP64 chain, as the reference), p95 by
+//                       nearest rank via an MSB radix select, MFU/MBU; plus
+//                       the additive p50/p99 TTFT/TPOT outputs.
+//  compact_kernel       per_request sorted by id / rejected_ids sorted
+//                       (simulator.cpp:205-207) as dense arrays for one D2H.
+//  rank_kernel          search()'s comparator (simulator.cpp:283-294):
+//                       (num_rejected, objective, other, encoding, freq).
+#include <cub/block/block_scan.cuh>
+
+#include "psg_device.cuh"
+#include "psg_reduce.cuh"
+
+namespace psg {
+
+namespace {
+
+__device__ __forceinline__ uint64_t order_key(double v) {
+  const uint64_t b = __double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_order_key(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(b);
+}
+
+// k-th smallest (0-based) value among slots passing `pred`, by 8 MSB-first
+// 8-bit radix passes with a shared histogram.  All threads of the CTA call it.
+template <typename Pred>
+__device__ double block_select(const double* __restrict__ v, int64_t n, int64_t k,
+                               Pred pred, unsigned* hist, uint64_t* shared_prefix,
+                               int64_t* shared_k) {
+  uint64_t prefix = 0, mask = 0;
+  if (threadIdx.x == 0) *shared_k = k;
+  for (int pass = 7; pass >= 0; --pass) {
+    const int shift = pass * 8;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      if (!pred(i)) continue;
+      const uint64_t key = order_key(v[i]);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t kk = *shared_k;
+      int d = 0;
+      for (; d < 255; ++d) {
+        if (kk < int64_t(hist[d])) break;
+        kk -= hist[d];
+      }
+      *shared_k = kk;
+      *shared_prefix = prefix | (uint64_t(d) << shift);
+    }
+    __syncthreads();
+    prefix = *shared_prefix;
+    mask |= uint64_t(255) << shift;
+    __syncthreads();
+  }
+  return from_order_key(prefix);
+}
+
+// Nearest-rank index of simulator.cpp:224-225.
+__device__ __forceinline__ int64_t nearest_rank(double q, int64_t n) {
+  const int64_t rank = int64_t(ceil(__dmul_rn(q, double(n))));
+  const int64_t idx = rank == 0 ? 0 : rank - 1;
+  return idx < n - 1 ? idx : n - 1;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r) {
+  const int e = blockIdx.x;
+  __shared__ unsigned hist[256];
+  __shared__ uint64_t sh_prefix;
+  __shared__ int64_t sh_k;
+  __shared__ double sh_sums[2];
+  __shared__ int64_t sh_cnt[2];
+
+  const size_t base = size_t(e) * size_t(r.n_slots);
+  const uint8_t* st = r.slot_status + base;
+  const double* ttft = r.slot_ttft + base;
+  const double* tpot = r.slot_tpot + base;
+  const double* e2e = r.slot_e2e + base;
+  const int64_t* gen = r.slot_gen;  // per slot (id order), shared by entries
+
+  // ---- ordered means: one serial chain in ascending id order (warp 0) ----
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double ts = 0.0, ps = 0.0;
+    int64_t pn = 0, cn = 0;
+    for (int64_t b0 = 0; b0 < r.n_slots; b0 += 32) {
+      const int64_t i = b0 + lane;
+      const bool c = i < r.n_slots && st[i] == 1;
+      const double tv = c ? ttft[i] : 0.0;
+      const bool g2 = c && gen[i] >= 2;
+      const double pv = g2 ? tpot[i] : 0.0;
+      unsigned cm = __ballot_sync(0xffffffffu, c);
+      const unsigned gm = __ballot_sync(0xffffffffu, g2);
+      cn += __popc(cm);
+      pn += __popc(gm);
+      while (cm) {
+        const int l = __ffs(cm) - 1;
+        cm &= cm - 1;
+        ts = __dadd_rn(ts, __shfl_sync(0xffffffffu, tv, l));
+        if ((gm >> l) & 1u) ps = __dadd_rn(ps, __shfl_sync(0xffffffffu, pv, l));
+      }
+    }
+    if (lane == 0) {
+      sh_sums[0] = ts;
+      sh_sums[1] = ps;
+      sh_cnt[0] = cn;
+      sh_cnt[1] = pn;
+    }
+  }
+  __syncthreads();
+  const int64_t ncomp = sh_cnt[0], ntpot = sh_cnt[1];
+
+  EntryOut o;
+  if (threadIdx.x == 0) {
+    o.e2e = 0.0;
+    o.energy = 0.0;
+    o.flops = 0.0;
+    o.bytes = 0.0;
+    o.iterations = 0;
+    o.max_batch = 0;
+    o.rejected = 0;
+    o.err = 0;
+    for (int k = r.entry_unit_begin[e]; k < r.entry_unit_begin[e + 1]; ++k) {
+      const UnitOut& u = r.uout[r.entry_units[k]];
+      o.e2e = o.e2e < u.clock ? u.clock : o.e2e;
+      o.energy = __dadd_rn(o.energy, u.energy);
+      o.flops = __dadd_rn(o.flops, u.flops);
+      o.bytes = __dadd_rn(o.bytes, u.bytes);
+      o.iterations += u.iterations;
+      o.max_batch = o.max_batch > u.max_batch ? o.max_batch : u.max_batch;
+      o.rejected += u.rejected;
+      if (!o.err && u.err) o.err = u.err;
+    }
+    o.completed = ncomp;
+    o.mean_ttft = ncomp > 0 ? __ddiv_rn(sh_sums[0], double(ncomp)) : 0.0;
+    o.mean_tpot = ntpot > 0 ? __ddiv_rn(sh_sums[1], double(ntpot)) : 0.0;
+    o.mfu = 0.0;
+    o.mbu = 0.0;
+    if (o.e2e > 0) {
+      const double pf = r.entry_peak[e];
+      if (!(pf > 0)) {
+        if (!o.err) o.err = 3;  // peak_flops_for() throws DataError
+      } else {
+        o.mfu = __ddiv_rn(o.flops, __dmul_rn(o.e2e, pf));
+        o.mbu = __ddiv_rn(o.bytes, __dmul_rn(__dmul_rn(o.e2e, r.mem_bw),
+                                             double(r.total_devices)));
+      }
+    }
+  }
+
+  // ---- order statistics ----
+  double p95 = 0.0, t50 = 0.0, t99 = 0.0, q50 = 0.0, q99 = 0.0;
+  if (ncomp > 0) {
+    auto done = [&](int64_t i) { return st[i] == 1; };
+    auto done2 = [&](int64_t i) { return st[i] == 1 && gen[i] >= 2; };
+    p95 = block_select(e2e, r.n_slots, nearest_rank(0.95, ncomp), done, hist, &sh_prefix, &sh_k);
+    if (r.extras) {
+      t50 = block_select(ttft, r.n_slots, nearest_rank(0.50, ncomp), done, hist, &sh_prefix, &sh_k);
+      t99 = block_select(ttft, r.n_slots, nearest_rank(0.99, ncomp), done, hist, &sh_prefix, &sh_k);
+      if (ntpot > 0) {
+        q50 = block_select(tpot, r.n_slots, nearest_rank(0.50, ntpot), done2, hist, &sh_prefix, &sh_k);
+        q99 = block_select(tpot, r.n_slots, nearest_rank(0.99, ntpot), done2, hist, &sh_prefix, &sh_k);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    o.p95 = p95;
+    o.p50_ttft = t50;
+    o.p99_ttft = t99;
+    o.p50_tpot = q50;
+    o.p99_tpot = q99;
+    r.eout[e] = o;
+    psg_rank_key k;
+    const bool lat = r.objective == PSG_OBJ_LATENCY;
+    k.num_rejected = o.rejected;
+    k.objective_metric = lat ? o.e2e : o.energy;
+    k.other_metric = lat ? o.energy : o.e2e;
+    k.enc_rank = r.entry_enc_rank[e];
+    k.pad_ = 0;
+    k.freq_ghz = r.entry_freq[e];
+    k.entry_index = r.entry_global[e];
+    r.keys[e] = k;
+  }
+}
+
+// Exclusive scan of per-entry completed / rejected counts (single CTA).
+__global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
+                               int64_t* rj_off, int64_t* totals) {
+  if (threadIdx.x != 0) return;
+  int64_t a = 0, b = 0;
+  for (int e = 0; e < n_entries; ++e) {
+    pr_off[e] = a;
+    rj_off[e] = b;
+    a += eout[e].completed;
+    b += eout[e].rejected;
+  }
+  totals[0] = a;
+  totals[1] = b;
+}
+
+// Dense per_request / rejected_ids in ascending id order per entry.
+__global__ void __launch_bounds__(256) compact_kernel(const ReduceParams r,
+                                                     const int64_t* pr_off,
+                                                     const int64_t* rj_off,
+                                                     psg_request_metrics* out_pr,
+                                                     int64_t* out_rj) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry[2];
+  const int e = blockIdx.x;
+  const size_t base = size_t(e) * size_t(r.n_slots);
+  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < r.n_slots; b0 += 256) {
+    const int64_t i = b0 + threadIdx.x;
+    const uint8_t s = i < r.n_slots ? r.slot_status[base + i] : 0;
+    int c = s == 1, j = s == 2;
+    int cp, jp, ct, jt;
+    Scan(tmp).ExclusiveSum(c, cp, ct);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(j, jp, jt);
+    if (c) {
+      psg_request_metrics m;
+      m.id = r.slot_id[i];
+      m.ttft = r.slot_ttft[base + i];
+      m.tpot = r.slot_tpot[base + i];
+      m.e2e = r.slot_e2e[base + i];
+      m.gen_len = r.slot_gen[i];
+      out_pr[pr_off[e] + carry[0] + cp] = m;
+    }
+    if (j) out_rj[rj_off[e] + carry[1] + jp] = r.slot_id[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry[0] += ct;
+      carry[1] += jt;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ bool key_less(const psg_rank_key& a, const psg_rank_key& b) {
+  if (a.num_rejected != b.num_rejected) return a.num_rejected < b.num_rejected;
+  if (a.objective_metric != b.objective_metric) return a.objective_metric < b.objective_metric;
+  if (a.other_metric != b.other_metric) return a.other_metric < b.other_metric;
+  if (a.enc_rank != b.enc_rank) return a.enc_rank < b.enc_rank;
+  if (a.freq_ghz != b.freq_ghz) return a.freq_ghz < b.freq_ghz;
+  return a.entry_index < b.entry_index;  // total order (reference: unspecified)
+}
+
+// Rank by counting: pos(i) = #{j : key_j < key_i}.  Keys are tiled through
+// shared memory; the grid covers the entries in 256-wide blocks.
+__global__ void __launch_bounds__(256) rank_kernel(const psg_rank_key* keys, int64_t n,
+                                                   int64_t* order) {
+  __shared__ psg_rank_key tile[256];
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  psg_rank_key mine;
+  if (i < n) mine = keys[i];
+  int64_t pos = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += 256) {
+    if (t0 + threadIdx.x < n) tile[threadIdx.x] = keys[t0 + threadIdx.x];
+    __syncthreads();
+    const int m = int(n - t0 < 256 ? n - t0 : 256);
+    if (i < n)
+      for (int j = 0; j < m; ++j) pos += key_less(tile[j], mine);
+    __syncthreads();
+  }
+  if (i < n) order[pos] = i;
+}
+
+}  // namespace psg

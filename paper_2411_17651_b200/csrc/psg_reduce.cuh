@@ -1,0 +1,51 @@
+// psg_reduce.cuh — shared declarations of the engine's kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "psg.h"
+#include "psg_device.cuh"
+
+namespace psg {
+
+struct EntryOut {
+  double e2e, energy, flops, bytes, mean_ttft, mean_tpot, mfu, mbu, p95;
+  double p50_ttft, p99_ttft, p50_tpot, p99_tpot;
+  int64_t iterations, max_batch, completed, rejected;
+  int32_t err, pad;
+};
+
+struct ReduceParams {
+  int64_t n_slots;
+  const uint8_t* slot_status;
+  const double *slot_ttft, *slot_tpot, *slot_e2e;
+  const int64_t* slot_gen;   // gen_len by slot (id order)
+  const int64_t* slot_id;    // id by slot
+  const UnitOut* uout;
+  const int32_t* entry_unit_begin;  // [entries + 1]
+  const int32_t* entry_units;       // unit ids, replica order
+  const double* entry_peak;         // peak_flops_for(dtype) * total_devices
+  const int32_t* entry_enc_rank;
+  const double* entry_freq;
+  const int64_t* entry_global;      // global entry index
+  double mem_bw;
+  int32_t total_devices;
+  int32_t objective;
+  int32_t extras;
+  EntryOut* eout;
+  psg_rank_key* keys;
+};
+
+__global__ void sim_kernel(const SimParams p);
+__global__ void entry_reduce_kernel(const ReduceParams r);
+__global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
+                               int64_t* rj_off, int64_t* totals);
+__global__ void compact_kernel(const ReduceParams r, const int64_t* pr_off,
+                               const int64_t* rj_off, psg_request_metrics* out_pr,
+                               int64_t* out_rj);
+__global__ void rank_kernel(const psg_rank_key* keys, int64_t n, int64_t* order);
+
+size_t sim_smem_bytes(int smem_cap, int memo_cap);
+
+}  // namespace psg

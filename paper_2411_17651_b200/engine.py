@@ -1,0 +1,99 @@
+"""Python front end of the B200 engine: `Engine.search` == plansim::search.
+
+    eng = Engine(device=0)
+    res = eng.search(plans, cluster, store, trace, Config(objective="latency"))
+    res.entries      # ranked SearchEntry scalars (numpy structured, ENTRY_DTYPE)
+    res.report(k)    # k-th ranked entry's per_request / rejected_ids
+
+Everything runs through the C ABI of libpsg.so (include/psg.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from .errors import from_code
+from .inputs import Cluster, Config, Plans, Store, Trace
+
+
+class SearchResult:
+    """Copies (or, with copy=False, views valid until the next call on the
+    same Engine) of the library's result arrays."""
+
+    def __init__(self, res: abi.ResultC, copy: bool = True, encodings=None):
+        def view(addr, n, dtype):
+            if n == 0 or not addr:
+                return np.zeros(0, dtype=dtype)
+            buf = (C.c_char * (int(n) * dtype.itemsize)).from_address(addr)
+            a = np.frombuffer(buf, dtype=dtype)
+            return a.copy() if copy else a
+
+        self.entries = view(res.entries, res.n_entries, abi.ENTRY_DTYPE)
+        self.per_request = view(res.per_request, res.n_per_request, abi.METRICS_DTYPE)
+        self.rejected_ids = view(res.rejected_ids, res.n_rejected, np.dtype("<i8"))
+        self.compute_clamp = view(res.compute_clamp, res.n_compute, np.dtype("u1"))
+        self.curve_clamp = view(res.curve_clamp, res.n_curves, np.dtype("u1"))
+        self.gpu_launches = int(res.gpu_launches)
+        self.total_iterations = int(res.total_iterations)
+        self.ms = {"total": res.ms_total, "h2d": res.ms_h2d, "sim": res.ms_sim,
+                   "reduce": res.ms_reduce, "d2h": res.ms_d2h}
+        self.encodings = encodings
+
+    def __len__(self):
+        return len(self.entries)
+
+    def report(self, k: int):
+        """(per_request, rejected_ids) of the k-th entry."""
+        e = self.entries[k]
+        o, n = int(e["per_request_offset"]), int(e["num_completed"])
+        ro, rn = int(e["rejected_offset"]), int(e["num_rejected"])
+        return self.per_request[o:o + n], self.rejected_ids[ro:ro + rn]
+
+    def encoding(self, k: int) -> str:
+        return self.encodings[int(self.entries[k]["plan_index"])]
+
+
+class Engine:
+    def __init__(self, device: int = 0):
+        self.lib = abi.load_library()
+        h = C.c_void_p()
+        rc = self.lib.psg_context_create(int(device), C.byref(h))
+        if rc != abi.PSG_OK:
+            raise from_code(rc, f"psg_context_create(device={device}) failed (rc={rc})")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            self.lib.psg_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, plans: Plans, cluster: Cluster, store: Store, trace: Trace,
+               config: Config | None = None, copy: bool = True) -> SearchResult:
+        config = config or Config()
+        out = C.POINTER(abi.ResultC)()
+        rc = self.lib.psg_search(self.handle, C.byref(plans.struct), C.byref(cluster.struct),
+                                 C.byref(store.struct), C.byref(trace.struct),
+                                 C.byref(config.struct), C.byref(out))
+        if rc != abi.PSG_OK:
+            raise from_code(rc, self.lib.psg_last_error(self.handle).decode())
+        try:
+            return SearchResult(out.contents, copy=copy, encodings=plans.encodings)
+        finally:
+            self.lib.psg_result_free(out)
+
+    def rank_keys(self, keys: np.ndarray) -> np.ndarray:
+        """Device ranking of gathered psg_rank_key records (multi-GPU merge)."""
+        keys = np.ascontiguousarray(keys, dtype=abi.RANK_KEY_DTYPE)
+        order = np.zeros(len(keys), dtype=np.int64)
+        rc = self.lib.psg_rank_keys(self.handle, keys.ctypes.data, len(keys), order.ctypes.data)
+        if rc != abi.PSG_OK:
+            raise from_code(rc, self.lib.psg_last_error(self.handle).decode())
+        return order

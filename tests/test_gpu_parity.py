@@ -1,0 +1,50 @@
+"""GPU engine vs the compiled reference (oracle/_ref/refdrv) on BASELINE.json's
+configurations: every ranked entry, every SimulationReport field, every
+per-request metric and rejected id must match bit for bit (MFU/MBU within
+1e-9 relative: per-replica tally partials)."""
+import pytest
+
+import pyoracle
+from harness import RefCase, compare_to_ref
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("c1", ()),
+    ("c3", ()),
+    ("c4", ()),
+    ("c4e", ()),
+    ("c1", ("--batching", "chunked", "--chunk", "128")),
+    ("c4", ("--max-batch", "8", "--anchor", "admission")),
+    ("c3", ("--batching", "chunked", "--chunk", "512", "--max-batch", "16")),
+]
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("key,extra", CASES, ids=[k + "".join(e) for k, e in CASES])
+def test_search_matches_reference(engine, workdir, key, extra):
+    case = RefCase(key, workdir, extra)
+    kw = {}
+    if "--batching" in extra:
+        kw["batching"] = extra[extra.index("--batching") + 1]
+    if "--chunk" in extra:
+        kw["chunk_size"] = int(extra[extra.index("--chunk") + 1])
+    if "--max-batch" in extra:
+        kw["max_batch_size"] = int(extra[extra.index("--max-batch") + 1])
+    if "--anchor" in extra:
+        kw["ttft_anchor"] = extra[extra.index("--anchor") + 1]
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config(**kw))
+    bad = compare_to_ref(res, case.ref, tally_rtol=1e-9)
+    assert not bad, "\n".join(bad)
+    assert res.total_iterations == case.line["plan_iterations"]
+    assert res.gpu_launches >= 4
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("key", ["c2", "c2fp8"])
+def test_c2_matches_reference(engine, workdir, key):
+    case = RefCase(key, workdir)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=1e-9)
+    assert not bad, "\n".join(bad)
