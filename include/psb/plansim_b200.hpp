@@ -218,7 +218,10 @@ class ProfileStore {
   bool has_compute_table(OpKind op, Dtype dt, double freq_ghz) const;
   // Flat structure-of-arrays view for the engine (valid while *this lives
   // and is not modified).
-  const psg_store& view() const { return view_; }
+  const psg_store& view() const {
+    rebind();
+    return view_;
+  }
   // Clamp-warning log (cost.cpp:191-194): reproduced from the engine's
   // per-table clamp flags after a search.
   std::vector<std::string> warnings() const { return warnings_; }
@@ -234,7 +237,8 @@ class ProfileStore {
   std::vector<int32_t> c_op_, c_dt_, c_nc_, c_nt_, c_nw_, k_kind_, k_dev_, k_nodes_, k_n_;
   std::vector<int64_t> c_fm_, c_kb_, c_vb_, k_b_;
   std::vector<double> c_knots_, c_sec_, c_jou_, k_pay_, k_sec_, k_jou_;
-  psg_store view_{};
+  mutable psg_store view_{};
+  void rebind() const;  // points view_ at this object's storage (copy-safe)
   mutable std::vector<std::string> warnings_;
   mutable std::vector<std::string> warn_keys_;
 };

@@ -1,0 +1,354 @@
+// Plan enumeration, device mapping, collective resolution and the memory
+// ledger: the producer of the engine's plan SoA.  Semantics follow
+// /root/reference/proj/src/planner.cpp:15-418 (Alg. 1 of the APEX paper),
+// verified field-for-field against the reference's plan dump in
+// tests/test_host_planner.py.
+#include <algorithm>
+#include <iostream>
+#include <set>
+#include <sstream>
+
+#include "nlohmann/json.hpp"
+#include "psb/plansim_b200.hpp"
+
+namespace psb {
+
+const char* op_kind_str(OpKind k) {
+  switch (k) {
+    case OpKind::Attention: return "attention";
+    case OpKind::GEMM: return "gemm";
+    case OpKind::MoEGEMM: return "moe_gemm";
+  }
+  return "?";
+}
+
+const char* collective_kind_str(CollectiveKind k) {
+  switch (k) {
+    case CollectiveKind::AllReduce: return "allreduce";
+    case CollectiveKind::AllGather: return "allgather";
+    case CollectiveKind::ReduceScatter: return "reduce_scatter";
+    case CollectiveKind::AllToAll: return "all_to_all";
+    case CollectiveKind::P2P: return "p2p";
+  }
+  return "?";
+}
+
+bool template_valid(const CellSpec& cell, int devices, ParallelMode mode) {
+  if (devices < 1) return false;
+  if (mode == ParallelMode::EP)
+    return cell.kind == CellKind::MoE && devices <= cell.num_experts &&
+           cell.num_experts % devices == 0;
+  const int granularity = cell.kind == CellKind::MoE ? cell.tp_slices : cell.num_tasks;
+  return granularity % devices == 0;
+}
+
+namespace {
+
+// Per-device weight bytes of one cell shard (planner.cpp:26-71).
+double shard_weight_bytes(const CellSpec& cell, int devices, ParallelMode mode) {
+  if (!template_valid(cell, devices, mode))
+    throw DataError(std::string("template: cannot split ") + cell_kind_str(cell.kind) +
+                    " cell across " + std::to_string(devices) + " devices");
+  if (mode == ParallelMode::EP || cell.kind == CellKind::MoE || !cell.is_attention())
+    return cell.weight_bytes() / devices;
+  // query heads shard evenly; kv heads shard until the split outruns them,
+  // after which every shard keeps one replicated kv head
+  const int heads_here = cell.num_tasks / devices;
+  const double kv_here = cell.kv_heads >= devices ? double(cell.kv_heads) / devices : 1.0;
+  return heads_here * cell.qo_weight_bytes_per_task + kv_here * cell.kv_weight_bytes_per_kv_head;
+}
+
+CellScheme cell_scheme(const CellSpec& cell, ParallelMode mode, int cell_dp, int intra) {
+  CellScheme s;
+  s.cell = cell;
+  s.mode = intra == 1 ? ParallelMode::TP : mode;  // EP over one device is TP
+  s.cell_dp = cell_dp;
+  s.intra_degree = intra;
+  s.weight_bytes_per_device = shard_weight_bytes(cell, intra, s.mode);
+  s.query_width = cell.task_width;
+  const double token_split = 1.0 / cell_dp;
+  if (cell.kind == CellKind::MoE) {
+    s.op = OpKind::MoEGEMM;
+    const double routing = double(cell.experts_per_token) / cell.num_experts;
+    if (s.mode == ParallelMode::EP) {
+      s.query_tasks = double(cell.num_experts) / intra;
+      s.token_scale = token_split * routing;
+    } else {  // every expert sliced 1/intra; the slice folds into the token axis
+      s.query_tasks = double(cell.num_experts);
+      s.token_scale = token_split * routing / intra;
+    }
+  } else {
+    s.op = cell.is_attention() ? OpKind::Attention : OpKind::GEMM;
+    s.query_tasks = double(cell.num_tasks) / intra;
+    s.token_scale = token_split;
+  }
+  return s;
+}
+
+// Reshard collectives between adjacent cells (planner.cpp:121-152).
+std::vector<CollectiveOp> reshard(const CellScheme& l, const CellScheme& r, const ModelSpec& m) {
+  const double per_token = double(m.hidden_size) * m.activation_dtype.bytes_per_element;
+  const bool l_ep = l.mode == ParallelMode::EP && l.intra_degree > 1;
+  const bool r_ep = r.mode == ParallelMode::EP && r.intra_degree > 1;
+  std::vector<CollectiveOp> ops;
+  auto add = [&](CollectiveKind k, double share, GroupScope scope) {
+    ops.push_back({k, per_token, share, scope});
+  };
+  if (l_ep) add(CollectiveKind::AllToAll, 1.0 / l.cell_dp, GroupScope::LeftIntra);
+  if (r_ep) {
+    add(CollectiveKind::AllToAll, 1.0 / r.cell_dp, GroupScope::RightIntra);
+  } else if (l.cell_dp == r.cell_dp) {
+    if (!l_ep && l.intra_degree > 1)
+      add(CollectiveKind::AllReduce, 1.0 / l.cell_dp, GroupScope::LeftIntra);
+  } else {
+    add(CollectiveKind::AllToAll, 1.0, GroupScope::Stage);
+    if (r.intra_degree > 1) add(CollectiveKind::AllGather, 1.0 / r.cell_dp, GroupScope::RightIntra);
+  }
+  return ops;
+}
+
+ParallelScheme assemble(const ModelSpec& m, const BlockSpec& block, int dp, int stages, int sdev,
+                        std::vector<CellScheme> cells) {
+  ParallelScheme s;
+  s.model_dp = dp;
+  s.num_stages = stages;
+  s.stage_devices = sdev;
+  s.stage_repetitions = block.repeat_count / stages;
+  std::ostringstream enc;
+  enc << "dp" << dp << ":pp" << stages;
+  for (size_t i = 0; i < cells.size(); ++i) {
+    const CellScheme& c = cells[i];
+    enc << ":" << cell_kind_str(c.cell.kind) << (c.mode == ParallelMode::EP ? "-ep" : "-tp")
+        << c.intra_degree << "x" << c.cell_dp;
+    s.reshards.push_back(reshard(c, cells[(i + 1) % cells.size()], m));
+  }
+  s.cells = std::move(cells);
+  s.encoding = enc.str();
+  return s;
+}
+
+struct Span {
+  int devices = 0, nodes = 0, level = 0;
+};
+
+Span group_span(const ClusterSpec& cl, const std::vector<int>& ids) {
+  Span s;
+  s.devices = int(ids.size());
+  const int per_node = cl.devices_per_node();
+  std::set<int> nodes;
+  for (int id : ids) nodes.insert(id / per_node);
+  s.nodes = int(nodes.size());
+  s.level = cl.num_levels();
+  for (int level = 0; level <= cl.num_levels(); ++level) {
+    const int cap = cl.subtree_capacity(level);
+    if (std::all_of(ids.begin(), ids.end(), [&](int id) { return id / cap == ids.front() / cap; })) {
+      s.level = level;
+      break;
+    }
+  }
+  return s;
+}
+
+ExecutionPlan finalize(const ModelSpec& m, const ParallelScheme& scheme, const ClusterSpec& cl,
+                       const PlanOptions& opts) {
+  ExecutionPlan plan;
+  plan.scheme = scheme;
+  plan.assignment = map_devices(scheme.model_dp, scheme.num_stages, scheme.stage_devices, cl);
+  plan.compute_dtype = m.activation_dtype.name;
+  plan.op_shape.model_hidden = m.hidden_size;
+  plan.op_shape.head_dim = m.head_dim;
+  plan.op_shape.kv_elems_per_task_token =
+      2.0 * m.head_dim / (m.num_attention_heads / double(m.num_kv_heads));
+  plan.p2p_payload_per_token = double(m.hidden_size) * m.activation_dtype.bytes_per_element;
+
+  const size_t nc = scheme.cells.size();
+  for (size_t i = 0; i < nc; ++i) {
+    const CellScheme& l = scheme.cells[i];
+    const CellScheme& r = scheme.cells[(i + 1) % nc];
+    for (const CollectiveOp& op : scheme.reshards[i]) {
+      const int gsize = op.scope == GroupScope::LeftIntra    ? l.intra_degree
+                        : op.scope == GroupScope::RightIntra ? r.intra_degree
+                                                             : scheme.stage_devices;
+      if (gsize < 2) continue;  // single-device group: elided
+      ResolvedCollective rc;
+      rc.kind = op.kind;
+      rc.payload_bytes_per_token = op.payload_bytes_per_token;
+      rc.token_share = op.token_share;
+      rc.groups_per_stage = scheme.stage_devices / gsize;
+      // worst span over every concrete group instance (planner.cpp:251-274)
+      Span worst;
+      bool first = true;
+      std::vector<int> ids(static_cast<size_t>(gsize));
+      for (int rep = 0; rep < scheme.model_dp; ++rep)
+        for (int st = 0; st < scheme.num_stages; ++st)
+          for (int g = 0; g < rc.groups_per_stage; ++g) {
+            for (int j = 0; j < gsize; ++j)
+              ids[size_t(j)] = plan.assignment.device_of(rep, st, g * gsize + j);
+            const Span s = group_span(cl, ids);
+            if (first || s.level > worst.level || (s.level == worst.level && s.nodes > worst.nodes)) {
+              worst = s;
+              first = false;
+            }
+          }
+      rc.num_devices = worst.devices;
+      rc.num_nodes = worst.nodes;
+      if (rc.num_devices >= 2) plan.block_collectives.push_back(rc);
+    }
+  }
+
+  const int per_node = cl.devices_per_node();
+  for (int b = 0; b + 1 < scheme.num_stages; ++b) {
+    const int a = plan.assignment.device_of(0, b, 0), c = plan.assignment.device_of(0, b + 1, 0);
+    plan.p2p_boundary_nodes.push_back(a / per_node == c / per_node ? 1 : 2);
+  }
+
+  double per_device = 0.0;
+  for (const auto& cs : scheme.cells) per_device += cs.weight_bytes_per_device;
+  per_device *= scheme.stage_repetitions;
+  const double emb = opts.include_embedding ? embedding_weight_bytes(m) : 0.0;
+  double last_stage = per_device;
+  if (opts.include_embedding) last_stage += emb / scheme.stage_devices;
+  plan.static_bytes_per_device = std::max(per_device, last_stage);
+  const int replica_devices = scheme.num_stages * scheme.stage_devices;
+  const double replica_static =
+      per_device * replica_devices + (opts.include_embedding ? emb : 0.0);
+  const double replica_capacity = cl.device.memory_capacity * replica_devices;
+  plan.kv_budget_per_replica =
+      std::max(0.0, replica_capacity * (1.0 - opts.activation_reserve) - replica_static);
+  double per_layer = 0.0;
+  for (const auto& cs : scheme.cells) {
+    if (!cs.cell.is_attention()) continue;
+    const double kv_instances = std::max(double(cs.cell.kv_heads), double(cs.intra_degree));
+    per_layer += 2.0 * cs.cell.head_dim * kv_instances * m.kv_cache_dtype.bytes_per_element;
+  }
+  plan.kv_bytes_per_token = per_layer * m.num_layers;
+  return plan;
+}
+
+}  // namespace
+
+std::vector<ParallelScheme> enumerate_schemes(const ModelSpec& m, const BlockSpec& block, int n,
+                                              int max_combos) {
+  std::vector<ParallelScheme> out;
+  std::set<std::string> seen;
+  if (n < 1 || block.repeat_count < 1) return out;
+  for (const int dp : divisors(n)) {
+    const int per_replica = n / dp;
+    for (const int stages : divisors(per_replica)) {
+      if (stages > block.repeat_count || block.repeat_count % stages) continue;
+      const int s = per_replica / stages;
+      std::vector<std::vector<CellScheme>> choices(block.cells.size());
+      bool viable = true;
+      for (size_t ci = 0; ci < block.cells.size() && viable; ++ci) {
+        for (const int cdp : divisors(s)) {
+          const int intra = s / cdp;
+          if (template_valid(block.cells[ci], intra, ParallelMode::TP))
+            choices[ci].push_back(cell_scheme(block.cells[ci], ParallelMode::TP, cdp, intra));
+          if (intra > 1 && template_valid(block.cells[ci], intra, ParallelMode::EP))
+            choices[ci].push_back(cell_scheme(block.cells[ci], ParallelMode::EP, cdp, intra));
+        }
+        viable = !choices[ci].empty();
+      }
+      if (!viable) continue;
+      long long combos = 1;
+      for (const auto& c : choices) combos *= (long long)c.size();
+      if (combos > max_combos) {
+        std::cerr << "warning: capping cell-scheme combinations at " << max_combos << " (of "
+                  << combos << ") for dp=" << dp << " stages=" << stages << "\n";
+        combos = max_combos;
+      }
+      // mixed-radix counter over the per-cell choices, last cell fastest
+      std::vector<size_t> digit(block.cells.size(), 0);
+      for (long long k = 0; k < combos; ++k) {
+        std::vector<CellScheme> cells;
+        for (size_t ci = 0; ci < digit.size(); ++ci) cells.push_back(choices[ci][digit[ci]]);
+        ParallelScheme sch = assemble(m, block, dp, stages, s, std::move(cells));
+        if (seen.insert(sch.encoding).second) out.push_back(std::move(sch));
+        for (size_t ci = digit.size(); ci-- > 0;) {
+          if (++digit[ci] < choices[ci].size()) break;
+          digit[ci] = 0;
+        }
+      }
+    }
+  }
+  return out;
+}
+
+std::vector<ExecutionPlan> generate_plans(const ModelSpec& m, const BlockSpec& block,
+                                          const ClusterSpec& cl, const PlanOptions& opts) {
+  std::vector<ExecutionPlan> plans;
+  for (const auto& sch : enumerate_schemes(m, block, cl.total_devices(), opts.max_cell_combinations)) {
+    ExecutionPlan p = finalize(m, sch, cl, opts);
+    if (p.static_bytes_per_device <= cl.device.memory_capacity) plans.push_back(std::move(p));
+  }
+  if (plans.empty()) throw InfeasibleError("no parallel execution plan fits the model on this cluster");
+  return plans;
+}
+
+ExecutionPlan build_plan(const ModelSpec& m, const BlockSpec& block, const ClusterSpec& cl,
+                         int dp, int stages, const std::vector<CellChoice>& choices,
+                         const PlanOptions& opts) {
+  const int n = cl.total_devices();
+  if (dp < 1 || stages < 1 || n % (dp * stages) != 0)
+    throw DataError("plan: degrees do not divide the cluster device count");
+  const int s = n / (dp * stages);
+  if (block.repeat_count % stages != 0)
+    throw DataError("plan: stage count does not divide the layer count");
+  if (choices.size() != block.cells.size())
+    throw DataError("plan: cell scheme count does not match the block");
+  std::vector<CellScheme> cells;
+  for (size_t i = 0; i < choices.size(); ++i) {
+    const CellChoice& ch = choices[i];
+    if (ch.cell_dp * ch.intra_degree != s)
+      throw DataError("plan: cell_dp * intra_degree must equal stage devices");
+    if (!template_valid(block.cells[i], ch.intra_degree, ch.mode))
+      throw DataError("plan: invalid template for cell " +
+                      std::string(cell_kind_str(block.cells[i].kind)));
+    cells.push_back(cell_scheme(block.cells[i], ch.mode, ch.cell_dp, ch.intra_degree));
+  }
+  return finalize(m, assemble(m, block, dp, stages, s, std::move(cells)), cl, opts);
+}
+
+std::string plans_to_json(const std::vector<ExecutionPlan>& plans) {
+  using oj = nlohmann::ordered_json;
+  oj arr = oj::array();
+  for (const auto& p : plans) {
+    oj d;
+    d["encoding"] = p.scheme.encoding;
+    d["model_dp"] = p.scheme.model_dp;
+    d["num_stages"] = p.scheme.num_stages;
+    d["stage_devices"] = p.scheme.stage_devices;
+    d["stage_repetitions"] = p.scheme.stage_repetitions;
+    d["compute_dtype"] = int(p.compute_dtype);
+    d["kv_bytes_per_token"] = p.kv_bytes_per_token;
+    d["kv_budget_per_replica"] = p.kv_budget_per_replica;
+    d["static_bytes_per_device"] = p.static_bytes_per_device;
+    d["p2p_payload_per_token"] = p.p2p_payload_per_token;
+    d["shape"] = {p.op_shape.model_hidden, p.op_shape.head_dim, p.op_shape.kv_elems_per_task_token};
+    d["cells"] = oj::array();
+    for (const auto& c : p.scheme.cells)
+      d["cells"].push_back({{"kind", int(c.cell.kind)},
+                            {"mode", int(c.mode)},
+                            {"cell_dp", c.cell_dp},
+                            {"intra_degree", c.intra_degree},
+                            {"op", int(c.op)},
+                            {"query_tasks", c.query_tasks},
+                            {"query_width", c.query_width},
+                            {"token_scale", c.token_scale},
+                            {"weight_bytes_per_device", c.weight_bytes_per_device}});
+    d["collectives"] = oj::array();
+    for (const auto& rc : p.block_collectives)
+      d["collectives"].push_back({{"kind", int(rc.kind)},
+                                  {"payload_bytes_per_token", rc.payload_bytes_per_token},
+                                  {"token_share", rc.token_share},
+                                  {"num_devices", rc.num_devices},
+                                  {"num_nodes", rc.num_nodes},
+                                  {"groups_per_stage", rc.groups_per_stage}});
+    d["p2p_boundary_nodes"] = p.p2p_boundary_nodes;
+    d["assignment"] = p.assignment.phys;
+    arr.push_back(d);
+  }
+  return arr.dump() + "\n";
+}
+
+}  // namespace psb
