@@ -228,7 +228,15 @@ typedef struct psg_result {
   int64_t gpu_launches;               /* kernels launched by this call */
   int64_t total_iterations;           /* sum of num_iterations over entries */
   double ms_total;                    /* host wall time of the call */
-  double ms_h2d, ms_sim, ms_reduce, ms_d2h;  /* CUDA-event times of the phases */
+  double ms_h2d;                      /* CUDA-event time: input H2D + output clears */
+  double ms_sim;                      /* CUDA-event time: simulation kernel */
+  double ms_reduce;                   /* CUDA-event time: reduce + rank + compaction kernels */
+  double ms_d2h;                      /* CUDA-event time: result D2H copies */
+  int64_t h2d_bytes, d2h_bytes;       /* bytes copied host<->device by this call */
+  /* work counters behind the algorithmic-bytes roofline */
+  int64_t sum_batch;                  /* sum over all iterations of the batch size */
+  int64_t admissions;                 /* admissions, re-admissions included */
+  int64_t finishes;                   /* completed requests */
 } psg_result;
 
 typedef struct psg_context psg_context;

@@ -91,7 +91,9 @@ class ResultC(C.Structure):
                 ("n_curves", C.c_int32), ("curve_clamp", C.c_void_p),
                 ("gpu_launches", C.c_int64), ("total_iterations", C.c_int64),
                 ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_sim", C.c_double),
-                ("ms_reduce", C.c_double), ("ms_d2h", C.c_double)]
+                ("ms_reduce", C.c_double), ("ms_d2h", C.c_double), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64), ("sum_batch", C.c_int64), ("admissions", C.c_int64),
+                ("finishes", C.c_int64)]
 
 
 EXPORTED_SYMBOLS = ("psg_version", "psg_context_create", "psg_context_destroy",

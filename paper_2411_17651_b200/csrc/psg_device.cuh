@@ -65,6 +65,7 @@ struct Unit {
 struct UnitOut {
   double clock, energy, flops, bytes;
   int64_t iterations, max_batch, completed, rejected;
+  int64_t sum_batch, admissions;  // work counters (algorithmic bytes)
   int32_t err;         // 0 ok, 1 chunk_size < 1, 2 missing table
   int32_t pad;
 };

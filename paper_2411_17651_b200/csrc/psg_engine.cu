@@ -122,7 +122,7 @@ const char* dtype_name(int d) {
 struct psg_context {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj;
   HostBuf h_in, h_out, h_pr, h_rj;
@@ -575,6 +575,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaEventRecord(ctx->ev[3], st));
   // everything from uout onwards is small: one D2H
   PSG_CUDA(cudaMemcpyAsync(ctx->h_out.p, dw, wk.size, cudaMemcpyDeviceToHost, st));
+  PSG_CUDA(cudaEventRecord(ctx->ev[4], st));
   PSG_CUDA(cudaStreamSynchronize(st));
   const unsigned char* ho = static_cast<const unsigned char*>(ctx->h_out.p);
   auto H = [&](size_t off) { return ho + off; };
@@ -605,6 +606,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
 
   // ---- per-request arrays ----
   const int64_t n_pr = cfg->detail ? tot[0] : 0, n_rj = cfg->detail ? tot[1] : 0;
+  PSG_CUDA(cudaEventRecord(ctx->ev[5], st));
   if (cfg->detail) {
     PSG_CUDA(ctx->d_pr.ensure(std::max<int64_t>(n_pr, 1) * sizeof(psg_request_metrics)));
     PSG_CUDA(ctx->d_rj.ensure(std::max<int64_t>(n_rj, 1) * sizeof(int64_t)));
@@ -615,6 +617,9 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
                                       static_cast<int64_t*>(ctx->d_rj.p));
     ++launches;
     PSG_CUDA(cudaGetLastError());
+  }
+  PSG_CUDA(cudaEventRecord(ctx->ev[6], st));
+  if (cfg->detail) {
     if (n_pr)
       PSG_CUDA(cudaMemcpyAsync(ctx->h_pr.p, ctx->d_pr.p, n_pr * sizeof(psg_request_metrics),
                                cudaMemcpyDeviceToHost, st));
@@ -622,7 +627,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
       PSG_CUDA(cudaMemcpyAsync(ctx->h_rj.p, ctx->d_rj.p, n_rj * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, st));
   }
-  PSG_CUDA(cudaEventRecord(ctx->ev[4], st));
+  PSG_CUDA(cudaEventRecord(ctx->ev[7], st));
   PSG_CUDA(cudaStreamSynchronize(st));
 
   // ---- assemble result ----
@@ -669,18 +674,31 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   res->n_curves = S->n_curves;
   res->curve_clamp = ctx->curve_clamp.data();
   res->gpu_launches = launches;
-  int64_t iters = 0;
-  for (int e = 0; e < E; ++e) iters += eo[e].iterations;
+  int64_t iters = 0, sb = 0, adm = 0, fin = 0;
+  for (int e = 0; e < E; ++e) {
+    iters += eo[e].iterations;
+    sb += eo[e].sum_batch;
+    adm += eo[e].admissions;
+    fin += eo[e].completed;
+  }
   res->total_iterations = iters;
-  float ms = 0;
-  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-  res->ms_h2d = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
-  res->ms_sim = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
-  res->ms_reduce = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
-  res->ms_d2h = ms;
+  res->sum_batch = sb;
+  res->admissions = adm;
+  res->finishes = fin;
+  res->h2d_bytes = int64_t(in_bytes);
+  res->d2h_bytes = int64_t(wk.size) + n_pr * int64_t(sizeof(psg_request_metrics)) +
+                   n_rj * int64_t(sizeof(int64_t));
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+  res->ms_h2d = a;
+  cudaEventElapsedTime(&a, ctx->ev[1], ctx->ev[2]);
+  res->ms_sim = a;
+  cudaEventElapsedTime(&a, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&b, ctx->ev[5], ctx->ev[6]);
+  res->ms_reduce = double(a) + double(b);
+  cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&b, ctx->ev[6], ctx->ev[7]);
+  res->ms_d2h = double(a) + double(b);
   res->ms_total = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
   *out = res;
   return PSG_OK;

@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
     o.iterations = 0;
     o.max_batch = 0;
     o.rejected = 0;
+    o.sum_batch = 0;
+    o.admissions = 0;
     o.err = 0;
     for (int k = r.entry_unit_begin[e]; k < r.entry_unit_begin[e + 1]; ++k) {
       const UnitOut& u = r.uout[r.entry_units[k]];
@@ -139,6 +141,8 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
       o.iterations += u.iterations;
       o.max_batch = o.max_batch > u.max_batch ? o.max_batch : u.max_batch;
       o.rejected += u.rejected;
+      o.sum_batch += u.sum_batch;
+      o.admissions += u.admissions;
       if (!o.err && u.err) o.err = u.err;
     }
     o.completed = ncomp;

@@ -12,7 +12,7 @@ namespace psg {
 struct EntryOut {
   double e2e, energy, flops, bytes, mean_ttft, mean_tpot, mfu, mbu, p95;
   double p50_ttft, p99_ttft, p50_tpot, p99_tpot;
-  int64_t iterations, max_batch, completed, rejected;
+  int64_t iterations, max_batch, completed, rejected, sum_batch, admissions;
   int32_t err, pad;
 };
 

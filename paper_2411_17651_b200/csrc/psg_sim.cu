@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   const bool missing = p.entry_missing[U.entry] != 0;
 
   double clock = 0.0, energy = 0.0, flops = 0.0, bytes = 0.0;
-  int64_t n = 0, max_batch = 0, completed = 0, rejected = 0;
+  int64_t n = 0, max_batch = 0, completed = 0, rejected = 0, sum_batch = 0, admissions = 0;
   int B = 0, n_pre = 0, pend = 0, stack_top = 0;
   int64_t used = 0;          // KV ledger in tokens: sum(ctx + generated)
   int64_t next_fin = kNoFin;
@@ -415,6 +415,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       }
       ++B;
       ++n_pre;
+      ++admissions;
       used += ctx;
       if (stack_top > 0) --stack_top; else ++pend;
     }
@@ -459,6 +460,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       flops = __dadd_rn(flops, f);
       bytes = __dadd_rn(bytes, b);
       max_batch = max_batch > B ? max_batch : int64_t(B);
+      sum_batch += B;
       const int64_t n_new = n + 1;
       int64_t ncompl = 0, m = next_fin;
       for (int base = 0; base < B; base += kWarp) {
@@ -590,6 +592,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     }
     n += j;
     used += j * int64_t(B);
+    sum_batch += j * int64_t(B);
     if (j > 0) max_batch = max_batch > B ? max_batch : int64_t(B);
     if (!stop) finish_and_evict();
   }
@@ -606,6 +609,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     o.max_batch = max_batch;
     o.completed = completed;
     o.rejected = rejected;
+    o.sum_batch = sum_batch;
+    o.admissions = admissions;
     o.err = err;
     o.pad = 0;
     p.uout[blockIdx.x] = o;

@@ -39,6 +39,11 @@ class SearchResult:
         self.total_iterations = int(res.total_iterations)
         self.ms = {"total": res.ms_total, "h2d": res.ms_h2d, "sim": res.ms_sim,
                    "reduce": res.ms_reduce, "d2h": res.ms_d2h}
+        self.h2d_bytes = int(res.h2d_bytes)
+        self.d2h_bytes = int(res.d2h_bytes)
+        self.sum_batch = int(res.sum_batch)
+        self.admissions = int(res.admissions)
+        self.finishes = int(res.finishes)
         self.encodings = encodings
 
     def __len__(self):
