@@ -68,7 +68,9 @@ class _View:
         self.encodings = encodings
 
     def __len__(self):
-        return len(self.encodings) if self.encodings is not None else 0
+        if self.encodings is not None:
+            return len(self.encodings)
+        return int(getattr(self.struct, "n", 0))
 
 
 class Problem:

@@ -1,0 +1,173 @@
+"""Pins the CPU restatement oracle (oracle/restate.cpp):
+  1. against the reference's own known answers (hand-computed values from
+     test_simulator.cpp / test_batching.cpp, asserted here), and
+  2. bit for bit against the compiled reference (oracle/_ref/refdrv) on the
+     same input files: every named fixture, seeded random batching fixtures,
+     and the C1 / C4 configurations.
+Only then is the oracle trusted as the GPU engine's checker."""
+import math
+
+import numpy as np
+import pytest
+
+import catalog
+import pyoracle
+from cases import same_as_reference
+from harness import RefCase, compare_to_ref
+
+needs_ref = pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref not built")
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(catalog.NAMED))
+def test_oracle_matches_reference_on_fixture(workdir, name):
+    case = catalog.NAMED[name]()
+    rc, err, ref = case.reference(workdir, name)
+    assert rc == 0, err
+    same_as_reference(case.oracle(), ref)
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(40))
+def test_oracle_matches_reference_on_random_batching(workdir, seed):
+    case = catalog.random_batching(seed)
+    rc, err, ref = case.reference(workdir, f"rand{seed}")
+    assert rc == 0, err
+    res = case.oracle()
+    same_as_reference(res, ref)
+    e = res.entries[0]
+    assert e["num_completed"] + e["num_rejected"] == len(case.prob.trace)
+
+
+@needs_ref
+@pytest.mark.parametrize("key", ["c1", "c4e"])
+def test_oracle_matches_reference_on_config(workdir, key):
+    case = RefCase(key, workdir)
+    res = pyoracle.oracle_search(case.plans, case.cluster, case.store, case.trace, case.config())
+    assert compare_to_ref(res, case.ref) == []
+
+
+# ---- known answers (the reference's own hand-computed values) ----------------
+
+def rel(a, b, tol):
+    return abs(a - b) <= tol * max(abs(a), abs(b))
+
+
+def test_single_request_known_answer():
+    # test_simulator.cpp:81-104: prefill(100) = 0.03 s, decode(1) = 0.0003 s
+    e = catalog.single_request().oracle().entries[0]
+    assert e["num_iterations"] == 2
+    assert rel(e["e2e_latency"], 0.0303, 1e-12)
+    assert rel(e["total_energy"], 0.303, 1e-12)
+    pr = catalog.single_request().oracle().report(0)[0]
+    assert rel(pr["ttft"][0], 0.03, 1e-12) and rel(pr["tpot"][0], 0.0003, 1e-12)
+
+
+def test_empty_trace_is_all_zero():
+    e = catalog.empty_trace().oracle().entries[0]
+    for f in ("e2e_latency", "total_energy", "num_completed", "num_rejected", "mfu"):
+        assert e[f] == 0
+
+
+def test_pipeline_max_and_sum_rule():
+    # two stages of one layer: duration = block + p2p charged to stage 1,
+    # energy = stage 0 + stage 1 (test_simulator.cpp:106-128)
+    e = catalog.pipeline_two_stages().oracle().entries[0]
+    p2p = lambda b: (1 - (b - 1) / (1e9 - 1)) * 1e-12 + ((b - 1) / (1e9 - 1)) * 1e-3
+    want = (0.03 + p2p(1600.0)) + (0.0003 + p2p(16.0))
+    assert rel(e["e2e_latency"], want, 1e-12)
+    assert e["e2e_latency"] > 0.0303
+    assert rel(e["total_energy"], 2 * 0.303, 1e-12)
+
+
+def test_dp2_equals_one_replica_on_half_the_trace():
+    a = catalog.dp2_full().oracle().entries[0]
+    b = catalog.dp1_half().oracle().entries[0]
+    assert a["e2e_latency"] == b["e2e_latency"]
+    assert rel(a["total_energy"], 2 * b["total_energy"], 1e-12)
+    assert a["num_completed"] == 8
+
+
+def test_free_collectives_rank_full_tp_first():
+    r = catalog.free_collectives().oracle()
+    assert r.encoding(0) == "dp1:pp1:MHA-tp4x1:SwiGLU-tp4x1"
+
+
+def test_prohibitive_internode_allreduce_dethrones_tp16():
+    r = catalog.prohibitive_internode().oracle()
+    encs = [r.encoding(i) for i in range(len(r))]
+    assert "dp1:pp1:GQA-tp16x1:SwiGLU-tp16x1" in encs[1:]
+    assert not encs[0].startswith("dp1:pp1:")
+
+
+def test_energy_objective_never_exceeds_latency_winner():
+    lat = catalog.energy_vs_latency("latency", [2.0]).oracle().entries[0]
+    en = catalog.energy_vs_latency("energy", [0.8, 2.0]).oracle().entries[0]
+    assert en["total_energy"] <= lat["total_energy"]
+
+
+def test_time_scaling_preserves_rank_order():
+    a = catalog.time_scaled(1.0).oracle()
+    b = catalog.time_scaled(3.7).oracle()
+    assert [a.encoding(i) for i in range(len(a))] == [b.encoding(i) for i in range(len(b))]
+    assert np.allclose(b.entries["e2e_latency"], 3.7 * a.entries["e2e_latency"], rtol=1e-9, atol=0)
+
+
+def test_utilization_within_physical_bounds():
+    r = catalog.utilization().oracle()
+    n = len(catalog.utilization().prob.trace)
+    for k in range(len(r)):
+        e = r.entries[k]
+        assert 0 < e["mfu"] <= 1 and 0 < e["mbu"] <= 1
+        assert e["num_completed"] + e["num_rejected"] == n
+        pr = r.report(k)[0]
+        assert (pr["ttft"] >= 0).all()
+        assert (pr["tpot"][pr["gen_len"] >= 2] > 0).all()
+
+
+def test_ttft_anchor_switches_between_arrival_and_admission():
+    a = catalog.ttft_anchor("arrival").oracle().report(0)[0]
+    b = catalog.ttft_anchor("admission").oracle().report(0)[0]
+    assert a["ttft"][1] > b["ttft"][1]
+    assert a["ttft"][0] == b["ttft"][0]
+
+
+def test_contiguous_and_chunked_iteration_counts():
+    # ctx=100 gen=3 -> 3 iterations; chunk 32 -> prefill 32,32,32,4 + 1 decode
+    assert catalog.contiguous_schedule().oracle().entries[0]["num_iterations"] == 3
+    assert catalog.chunked_schedule().oracle().entries[0]["num_iterations"] == 5
+
+
+def test_overflow_evicts_and_readmits():
+    r = catalog.overflow_eviction().oracle()
+    e = r.entries[0]
+    assert e["num_completed"] == 2 and e["num_rejected"] == 0
+    # request 1 restarted after eviction: strictly more than the 20 + 1 a clean run needs
+    assert e["num_iterations"] > 21
+
+
+def test_lone_outgrowing_request_is_rejected():
+    r = catalog.lone_outgrowing().oracle()
+    e = r.entries[0]
+    assert e["num_completed"] == 0 and e["num_rejected"] == 1
+    assert list(r.report(0)[1]) == [0]
+
+
+def test_crafted_cluster_prefers_hybrid_over_tp16():
+    # acceptance criterion 5's ranking direction on the crafted 2x8 store
+    r = catalog.crafted_2x8().oracle()
+    encs = [r.encoding(i) for i in range(len(r))]
+    tp16 = encs.index("dp1:pp1:GQA-tp16x1:SwiGLU-tp16x1")
+    hybrid = next(i for i, e in enumerate(encs) if not e.startswith("dp1:pp1:"))
+    assert hybrid < tp16
+
+
+def test_nearest_rank_p95_rule():
+    r = catalog.utilization().oracle()
+    for k in range(len(r)):
+        pr = r.report(k)[0]
+        if len(pr) == 0:
+            continue
+        s = np.sort(pr["e2e"])
+        rank = math.ceil(0.95 * len(s))
+        assert r.entries[k]["p95_latency"] == s[min(len(s) - 1, max(rank, 1) - 1)]
