@@ -102,11 +102,14 @@ EXPORTED_SYMBOLS = ("psg_version", "psg_context_create", "psg_context_destroy",
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> C.CDLL:
-    """Loads the in-tree engine library; raises if it has not been built."""
+def load_library(path: str = None) -> C.CDLL:
+    """Loads the in-tree engine library; raises if it has not been built.
+    PSG_LIBRARY may name another in-tree build (dev: libpsg_prof.so)."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = os.path.join(PKG_DIR, os.environ.get("PSG_LIBRARY", "libpsg.so"))
     if not os.path.exists(path):
         raise RuntimeError(
             f"{path} is missing: build the CUDA engine with "

@@ -17,7 +17,9 @@ namespace psg {
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxCells = 8;      // cells per block (the reference IR emits 2)
-constexpr int kMaxClampSlots = 64;
+constexpr int kMaxClampSlots = 64;  // cells + collectives + p2p boundaries
+constexpr int kWindow = 32;         // prefetched upcoming requests per unit
+constexpr int kProfSlots = 16;      // phase-profile counters per unit (dev builds)
 
 // ---------------------------------------------------------------------------
 // Device views of the ABI inputs (all pointers are device pointers).
@@ -88,6 +90,9 @@ struct SimParams {
   int32_t anchor;
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
+  int32_t tab_smem;          // doubles of per-unit table staging in shared memory (0: global)
+  int32_t tab_cap;           // doubles of table staging a unit may need
+  double* g_tab;             // global staging fallback, tab_cap doubles per unit
   int64_t n_slots;           // requests per entry (== trace length)
   // outputs
   UnitOut* uout;
@@ -98,12 +103,15 @@ struct SimParams {
   uint32_t* clamp_compute;   // per compute grid, bit 2*axis + above
   uint32_t* clamp_curve;     // per curve, bit 0 below / bit 1 above
   // scratch (global fallback for large batches)
-  int32_t* g_i32;            // 6 int32 arrays per unit, stride n_req
-  double* g_f64;             // 2 double arrays per unit, stride n_req
+  unsigned long long* prof;  // PSG_PHASE_PROFILE builds: kProfSlots counters per unit
+  int32_t* g_i32;            // kGI32 int32 arrays per unit, stride n_req
+  double* g_f64;             // kGF64 8-byte arrays per unit, stride n_req
 };
 
 // ---------------------------------------------------------------------------
-// Interpolation primitives (cost.cpp:85-102, :214-234, :279).
+// Interpolation primitives (cost.cpp:85-102, :214-234, :279).  All table
+// pointers are generic: the simulation kernel stages each unit's tables in
+// shared memory (global memory only if they do not fit).
 
 struct AxisPos {
   int lo, hi;
@@ -113,74 +121,67 @@ struct AxisPos {
 
 // locate(): x <= first -> (0,0,t=0); x >= last -> (n-1,n-1,t=0);
 // else hi = upper_bound(x), lo = hi-1, t = (x-k[lo])/(k[hi]-k[lo]).
-__device__ __forceinline__ AxisPos locate(const double* __restrict__ k, int n, double x) {
+__device__ __forceinline__ AxisPos locate(const double* k, int n, double x) {
   AxisPos p;
   p.t = 0.0;
   p.clamp = 0;
-  const double first = __ldg(k);
+  const double first = k[0];
   if (x <= first) {
     p.lo = p.hi = 0;
     p.clamp = x < first ? -1 : 0;
     return p;
   }
-  const double last = __ldg(k + n - 1);
+  const double last = k[n - 1];
   if (x >= last) {
     p.lo = p.hi = n - 1;
     p.clamp = x > last ? 1 : 0;
     return p;
   }
-  // upper_bound over (0, n-1): first index with k[i] > x; k[0] <= x < k[n-1].
+  // upper_bound: first index with k[i] > x, knowing k[0] <= x < k[n-1]
   int lo = 0, hi = n - 1;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(k + mid) > x) hi = mid; else lo = mid;
+    if (k[mid] > x) hi = mid; else lo = mid;
   }
   p.lo = lo;
   p.hi = hi;
-  const double klo = __ldg(k + lo);
-  p.t = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(__ldg(k + hi), klo));
+  const double klo = k[lo];
+  p.t = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(k[hi], klo));
   return p;
 }
 
-// Per-cell constant coordinates: the (tasks, width) positions are fixed for a
-// (plan, cell), so they are located once per unit.
+constexpr int kMaxCombos = 4;  // nonzero (tasks, width) corner pairs of a cell
+
+// A compute grid collapsed for one cell: the (tasks, width) coordinates are
+// fixed per (plan, cell), so only the context axis varies per query.  The
+// nonzero (cj, ck) corners are kept in the reference's loop order with their
+// weights, and their values are gathered into vals[n_ctx][ncombo][2]
+// (seconds, joules interleaved).
 struct CellConst {
-  int table;          // compute grid index
+  int table;          // compute grid index (-1: missing)
   int op;
-  int n_ctx, n_tasks, n_width;
-  int64_t knot_begin, value_begin;
-  AxisPos pj, pk;
+  int n_ctx, ncombo;
+  const double* knots;  // ctx knots
+  const double* vals;   // [n_ctx][ncombo][2]
+  double wj[kMaxCombos], wk[kMaxCombos];
   double tasks, width, scale;
+  uint32_t clamp_tw;    // tasks/width clamp bits (2..5), reported on every query
 };
 
 // Trilinear sample with the reference's skip-zero-weight loop order:
-// acc += ((wi*wj)*wk)*v for ci, cj, ck in {0,1}.
-__device__ __forceinline__ void sample_grid(const DStore& S, const CellConst& c,
-                                            const AxisPos& pi, double& sec,
-                                            double& joule) {
-  const double* __restrict__ vs = S.c_seconds + c.value_begin;
-  const double* __restrict__ vj = S.c_joules + c.value_begin;
+// acc += ((wi*wj)*wk)*v over ci, then the (cj, ck) corners.
+__device__ __forceinline__ void sample_cell(const CellConst& c, const AxisPos& pi,
+                                            double& sec, double& joule) {
   double as = 0.0, aj = 0.0;
 #pragma unroll
   for (int ci = 0; ci < 2; ++ci) {
     const double wi = ci ? pi.t : __dsub_rn(1.0, pi.t);
     if (wi == 0.0) continue;
-    const int i = ci ? pi.hi : pi.lo;
-#pragma unroll
-    for (int cj = 0; cj < 2; ++cj) {
-      const double wj = cj ? c.pj.t : __dsub_rn(1.0, c.pj.t);
-      if (wj == 0.0) continue;
-      const int j = cj ? c.pj.hi : c.pj.lo;
-#pragma unroll
-      for (int ck = 0; ck < 2; ++ck) {
-        const double wk = ck ? c.pk.t : __dsub_rn(1.0, c.pk.t);
-        if (wk == 0.0) continue;
-        const int k = ck ? c.pk.hi : c.pk.lo;
-        const int64_t idx = (int64_t(i) * c.n_tasks + j) * c.n_width + k;
-        const double w = __dmul_rn(__dmul_rn(wi, wj), wk);
-        as = __dadd_rn(as, __dmul_rn(w, __ldg(vs + idx)));
-        aj = __dadd_rn(aj, __dmul_rn(w, __ldg(vj + idx)));
-      }
+    const double* v = c.vals + (ci ? pi.hi : pi.lo) * c.ncombo * 2;
+    for (int k = 0; k < c.ncombo; ++k) {
+      const double w = __dmul_rn(__dmul_rn(wi, c.wj[k]), c.wk[k]);
+      as = __dadd_rn(as, __dmul_rn(w, v[2 * k]));
+      aj = __dadd_rn(aj, __dmul_rn(w, v[2 * k + 1]));
     }
   }
   sec = as;
@@ -206,18 +207,23 @@ __device__ __forceinline__ double op_bytes(int op, double t, double k, double w,
   return b;
 }
 
-// Collective curve: (1-t)*s[lo] + t*s[hi] (cost.cpp:279, :290).
-__device__ __forceinline__ void sample_curve(const DStore& S, int curve, double x,
-                                             double& sec, double& joule, int& clamp) {
-  const int64_t b = __ldg(S.k_begin + curve);
-  const int n = __ldg(S.k_n + curve);
-  const AxisPos p = locate(S.k_payload + b, n, x);
+// A staged collective curve (payload knots, seconds, joules) with the
+// resolved collective's payload factors: payload = (ppt * tokens) * share,
+// energy multiplier = groups_per_stage (1 for p2p).
+struct CurveConst {
+  const double *x, *s, *j;
+  double ppt, share, emul;
+  int n, table;
+};
+
+// (1-t)*s[lo] + t*s[hi] (cost.cpp:279, :290).
+__device__ __forceinline__ void sample_curve(const CurveConst& c, double x, double& sec,
+                                             double& joule, int& clamp) {
+  const AxisPos p = locate(c.x, c.n, x);
   clamp = p.clamp;
   const double u = __dsub_rn(1.0, p.t);
-  sec = __dadd_rn(__dmul_rn(u, __ldg(S.k_seconds + b + p.lo)),
-                  __dmul_rn(p.t, __ldg(S.k_seconds + b + p.hi)));
-  joule = __dadd_rn(__dmul_rn(u, __ldg(S.k_joules + b + p.lo)),
-                    __dmul_rn(p.t, __ldg(S.k_joules + b + p.hi)));
+  sec = __dadd_rn(__dmul_rn(u, c.s[p.lo]), __dmul_rn(p.t, c.s[p.hi]));
+  joule = __dadd_rn(__dmul_rn(u, c.j[p.lo]), __dmul_rn(p.t, c.j[p.hi]));
 }
 
 }  // namespace psg

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -124,7 +125,7 @@ struct psg_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
-  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj;
+  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj, d_tab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
@@ -174,7 +175,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
-                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj})
+                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_tab, &ctx->d_prof})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj}) b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -315,8 +316,10 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   int64_t tok_total = 0;
   bool sorted = true;
   for (int64_t i = 0; i < N; ++i) {
-    if (T->context_len[i] < 0 || T->context_len[i] >= INT32_MAX || T->gen_len[i] >= INT32_MAX)
-      return fail(ctx, PSG_ERR_USAGE, "trace lengths outside the supported int32 range");
+    // 2^26-token bound keeps every per-warp token reduction inside 32 bits
+    if (T->context_len[i] < 0 || T->context_len[i] >= (int64_t(1) << 26) ||
+        T->gen_len[i] >= (int64_t(1) << 26))
+      return fail(ctx, PSG_ERR_USAGE, "trace lengths outside the supported range [0, 2^26)");
     tok_total += T->context_len[i] + std::max<int64_t>(T->gen_len[i], 1);
     if (i && T->arrival[i] < T->arrival[i - 1]) sorted = false;
   }
@@ -463,8 +466,26 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(ctx->h_in.ensure(in_bytes));
   PSG_CUDA(ctx->d_slot_f64.ensure(std::max<size_t>(slots, 1) * 3 * sizeof(double)));
   PSG_CUDA(ctx->d_slot_u8.ensure(std::max<size_t>(slots, 1)));
-  PSG_CUDA(ctx->d_scratch_i32.ensure(std::max<int64_t>(scratch_total, 1) * 6 * sizeof(int32_t)));
-  PSG_CUDA(ctx->d_scratch_f64.ensure(std::max<int64_t>(scratch_total, 1) * 3 * sizeof(double)));
+  PSG_CUDA(ctx->d_scratch_i32.ensure(std::max<int64_t>(scratch_total, 1) * kScratchI32 * sizeof(int32_t)));
+  PSG_CUDA(ctx->d_scratch_f64.ensure(std::max<int64_t>(scratch_total, 1) * kScratchF64 * sizeof(double)));
+  // per-unit table staging: shared memory when it fits, else a global region
+  size_t tab_cap = 1;
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F), f = int(ent[e] % F);
+    std::vector<int> nctx, ncurve;
+    for (int c = P->cell_begin[p]; c < P->cell_begin[p + 1]; ++c) {
+      const int t = cell_tab[size_t(f) * n_cells + c];
+      nctx.push_back(t >= 0 ? S->c_n_ctx[t] : 1);
+    }
+    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1]; ++k)
+      ncurve.push_back(coll_tab[k] >= 0 ? S->k_n[coll_tab[k]] : 1);
+    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b)
+      ncurve.push_back(p2p_tab[b] >= 0 ? S->k_n[p2p_tab[b]] : 1);
+    tab_cap = std::max(tab_cap, sim_tab_doubles(int(nctx.size()), nctx.data(), int(ncurve.size()),
+                                                ncurve.data()));
+  }
+  const int tab_smem = tab_cap * sizeof(double) <= 64 * 1024 ? int(tab_cap) : 0;
+  if (!tab_smem) PSG_CUDA(ctx->d_tab.ensure(tab_cap * sizeof(double) * std::max(n_units, 1)));
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
   Packer wk;  // offsets only
   const size_t w_uout = wk.add<UnitOut>(nullptr, n_units), w_eout = wk.add<EntryOut>(nullptr, E),
@@ -514,6 +535,9 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.anchor = cfg->ttft_anchor;
   sp.smem_cap = 256;
   sp.memo_cap = 256;
+  sp.tab_smem = tab_smem;
+  sp.tab_cap = int(tab_cap);
+  sp.g_tab = static_cast<double*>(ctx->d_tab.p);
   sp.n_slots = N;
   sp.uout = (UnitOut*)W(w_uout);
   double* slot_f = static_cast<double*>(ctx->d_slot_f64.p);
@@ -523,6 +547,13 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.slot_status = static_cast<uint8_t*>(ctx->d_slot_u8.p);
   sp.clamp_compute = (uint32_t*)W(w_cc);
   sp.clamp_curve = (uint32_t*)W(w_kc);
+  sp.prof = nullptr;
+  const char* prof_path = std::getenv("PSG_PHASE_PROFILE");
+  if (prof_path) {  // dev builds: per-unit phase counters dumped after the run
+    PSG_CUDA(ctx->d_prof.ensure(sizeof(unsigned long long) * kProfSlots * std::max(n_units, 1)));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_prof.p, 0, sizeof(unsigned long long) * kProfSlots * std::max(n_units, 1), ctx->stream));
+    sp.prof = static_cast<unsigned long long*>(ctx->d_prof.p);
+  }
   sp.g_i32 = static_cast<int32_t*>(ctx->d_scratch_i32.p);
   sp.g_f64 = static_cast<double*>(ctx->d_scratch_f64.p);
 
@@ -555,7 +586,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaMemsetAsync(sp.slot_status, 0, std::max<size_t>(slots, 1), st));
   PSG_CUDA(cudaMemsetAsync(W(w_cc), 0, wk.size - w_cc, st));
   PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
-  const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap);
+  const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem);
   PSG_CUDA(cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (n_units > 0) {
     sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
@@ -630,6 +661,18 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaEventRecord(ctx->ev[7], st));
   PSG_CUDA(cudaStreamSynchronize(st));
 
+  if (prof_path) {
+    std::vector<unsigned long long> pr(size_t(kProfSlots) * n_units);
+    cudaMemcpy(pr.data(), ctx->d_prof.p, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(prof_path, "wb")) {
+      for (int u = 0; u < n_units; ++u) {  // unit -> (global entry, replica, counters)
+        const long long meta[2] = {(long long)ent[units[u].entry], (long long)units[u].replica};
+        std::fwrite(meta, sizeof meta, 1, f);
+        std::fwrite(pr.data() + size_t(u) * kProfSlots, sizeof(unsigned long long), kProfSlots, f);
+      }
+      std::fclose(f);
+    }
+  }
   // ---- assemble result ----
   ctx->entries.resize(E);
   for (int k = 0; k < E; ++k) {

@@ -8,18 +8,22 @@
 //  * Scalar state is warp-uniform (every lane holds the same clock/energy),
 //    so there is no broadcast; batch scans (finish compaction, prefill
 //    advance, min-finish) are lane-parallel over the active list with
-//    ballot/popc prefix compaction that keeps admission order.
-//  * The active list lives in shared memory (SoA, conflict-free lane access)
-//    and migrates to a per-unit global region if the batch outgrows it.
+//    ballot/popc compaction that keeps admission order and REDUX reductions.
+//  * Everything a unit touches per event lives in shared memory: the active
+//    list (SoA; migrates to a global region only if the batch outgrows it),
+//    a 32-request prefetch window of the replica's upcoming arrivals, and its
+//    cost tables — each cell's compute grid collapsed to the context axis at
+//    the cell's fixed (tasks, width) corners, each collective / distinct p2p
+//    curve — staged once at unit start.
 //  * Exact event-driven macro-stepping: a decode-only iteration's workload is
 //    {decode_count = B}, so its (seconds, joules, flops, bytes) are bit-
 //    identical until the batch changes.  Between events (arrival of an
 //    admissible/rejectable head, first finish, first KV overflow) the unit
 //    runs a tight loop of the reference's sequential FP64 adds only.
 //  * Costs: per-query locate/interpolate is lane-parallel; accumulation is
-//    serial in the reference's order (cells → items in admission order →
+//    serial in the reference's order (cells -> items in admission order ->
 //    decode, then collectives, then per-stage p2p), never a tree reduction.
-//  * A shared-memory memo caches decode-only costs per batch size.
+//    A shared-memory memo caches decode-only costs per batch size.
 #include <climits>
 
 #include "psg_device.cuh"
@@ -28,59 +32,94 @@ namespace psg {
 
 namespace {
 
-constexpr int64_t kNoFin = INT64_MAX;
-
-__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-
-__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t w = __shfl_xor_sync(kFull, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
-}
+constexpr int64_t kNoFin = INT64_MAX;   // prefill phase
+constexpr int64_t kDead = INT64_MIN;    // tombstone (finished / evicted slot)
+constexpr unsigned kNoRel = 0xffffffffu;
+constexpr int kGI32 = 7;  // global fallback arrays: stack, tidx, ctx, gen, done, slot, items
+constexpr int kGF64 = 4;  // adm, ft, arr, fin
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
   return (a < b) ? b : a;  // std::max(a, b)
 }
 
-// Active list: SoA over generic pointers (shared memory, or global after
-// migration).
-struct ActiveList {
-  int32_t *tidx, *ctx, *gen, *done, *items;
-  int64_t* fin;  // iteration index of the finishing decode step; kNoFin while prefilling
-  double *adm, *ft;
-};
-
 struct PlanConst {
   double kv, cap, reps, sdd, Sd, p2p_ppt, hidden, head_dim, kv_elems;
-  int S, C, K, NB, c0, k0, b0;
+  int S, C, K, NB, ND, c0, k0, b0;
 };
 
-// Lane-parallel query evaluation + reference-ordered serial accumulation.
-// Returns the iteration's duration (max over stages), energy (sum over
-// stages, in stage order) and the tally increments.
-__device__ void eval_iteration(const SimParams& p, const PlanConst& pc,
-                               const CellConst* __restrict__ cc,
-                               const int32_t* items, int n_items, int64_t decode,
-                               int64_t total, double* qv, uint32_t* clampbits,
-                               double& dur, double& energy, double& dflops,
-                               double& dbytes) {
+struct ActiveList {
+  int32_t *tidx, *ctx, *gen, *done, *slot, *items;
+  int64_t* fin;  // iteration index of the finishing decode step; kNoFin while prefilling
+  double *adm, *ft, *arr;
+};
+
+struct Cost {
+  double dur, energy, flops, bytes;
+};
+
+// Phase profiler (dev builds only: -DPSG_PHASE_PROFILE; zero code otherwise).
+// slots: 0 admit, 1 mixed scan, 2 mixed eval, 3 mixed advance, 4 decode cost,
+// 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
+// 11 #decode runs, 12 #decode evals, 13 #finish events, 14 unused, 15 total.
+#ifdef PSG_PHASE_PROFILE
+#define PROF_T0(v) const long long v = clock64()
+#define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
+#define PROF_CNT(slot) (prof_acc[slot] += 1ull)
+#else
+#define PROF_T0(v)
+#define PROF_ADD(slot, v)
+#define PROF_CNT(slot)
+#endif
+
+__host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct SmemLayout {
+  size_t qv, pc, cc, cv, p2p_slot, p2p_val, combo, clamp, win_arr, win_i32, memo, act_f64,
+      act_fin, act_i32, tab, total;
+};
+
+__host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem) {
+  SmemLayout L;
+  size_t o = 0;
+  L.qv = o;        o = al16(o + sizeof(double) * 4 * kWarp);
+  L.pc = o;        o = al16(o + sizeof(PlanConst));
+  L.cc = o;        o = al16(o + sizeof(CellConst) * kMaxCells);
+  L.cv = o;        o = al16(o + sizeof(CurveConst) * kMaxClampSlots);
+  L.p2p_slot = o;  o = al16(o + kMaxClampSlots);
+  L.p2p_val = o;   o = al16(o + sizeof(double) * 2 * kMaxClampSlots);
+  L.combo = o;     o = al16(o + sizeof(int32_t) * kMaxCells * kMaxCombos);
+  L.clamp = o;     o = al16(o + sizeof(uint32_t) * kMaxClampSlots);
+  L.win_arr = o;   o = al16(o + sizeof(double) * kWindow);
+  L.win_i32 = o;   o = al16(o + sizeof(int32_t) * 4 * kWindow);
+  L.memo = o;      o = al16(o + sizeof(double) * 4 * size_t(memo_cap));
+  L.act_f64 = o;   o = al16(o + sizeof(double) * 3 * size_t(smem_cap));
+  L.act_fin = o;   o = al16(o + sizeof(int64_t) * size_t(smem_cap));
+  L.act_i32 = o;   o = al16(o + sizeof(int32_t) * 6 * size_t(smem_cap));
+  L.tab = o;       o = al16(o + sizeof(double) * size_t(tab_smem));
+  L.total = o;
+  return L;
+}
+
+// Lane-parallel query evaluation + reference-ordered serial accumulation of
+// one iteration (iteration_time, simulator.cpp:17-87).  Kept out of line: the
+// kernel calls it from the mixed and the decode path, and the instruction
+// cache is the scarcer resource for one-warp-per-SMSP latency-bound code.
+__device__ __noinline__ Cost eval_iteration(const PlanConst* __restrict__ pc,
+                                            const CellConst* __restrict__ cc,
+                                            const CurveConst* __restrict__ cv,
+                                            const uint8_t* __restrict__ p2p_slot,
+                                            double* p2p_val, const int32_t* items,
+                                            int n_items, int64_t decode, int64_t total,
+                                            double* qv, uint32_t* clampbits) {
   const int lane = threadIdx.x;
+  const int C = pc->C, K = pc->K, ND = pc->ND;
   const int nq_c = n_items + (decode > 0 ? 1 : 0);
-  const int Qc = pc.C * nq_c;
-  const int Q = Qc + pc.K + pc.NB;
+  const int Qc = C * nq_c;
+  const int Q = Qc + K + ND;
   const double total_d = double(total);
+  const double sdd = pc->sdd;
 
   double bs = 0.0, bj = 0.0, bf = 0.0, bb = 0.0;
-  double srep = 0.0, jrep = 0.0, d = 0.0, e = 0.0;
-  bool staged = false;
-
   for (int base = 0; base < Q; base += kWarp) {
     const int q = base + lane;
     if (q < Q) {
@@ -91,33 +130,27 @@ __device__ void eval_iteration(const SimParams& p, const PlanConst& pc,
         const int64_t tok = i < n_items ? int64_t(items[i]) : decode;
         const CellConst& cell = cc[c];
         const double x = __dmul_rn(double(tok), cell.scale);
-        const AxisPos pi =
-            locate(p.S.c_knots + cell.knot_begin, cell.n_ctx, x);
-        sample_grid(p.S, cell, pi, t, en);
-        en = __dmul_rn(en, pc.sdd);  // query_energy * stage_devices
-        fl = op_flops(cell.op, x, cell.tasks, cell.width, pc.hidden, pc.head_dim);
-        by = op_bytes(cell.op, x, cell.tasks, cell.width, pc.hidden, pc.kv_elems);
-        const uint32_t bits = (pi.clamp < 0 ? 1u : 0u) | (pi.clamp > 0 ? 2u : 0u) |
-                              uint32_t(cell.pj.clamp < 0) << 2 |
-                              uint32_t(cell.pj.clamp > 0) << 3 |
-                              uint32_t(cell.pk.clamp < 0) << 4 |
-                              uint32_t(cell.pk.clamp > 0) << 5;
+        const AxisPos pi = locate(cell.knots, cell.n_ctx, x);
+        sample_cell(cell, pi, t, en);
+        en = __dmul_rn(en, sdd);  // query_energy * stage_devices
+        fl = op_flops(cell.op, x, cell.tasks, cell.width, pc->hidden, pc->head_dim);
+        by = op_bytes(cell.op, x, cell.tasks, cell.width, pc->hidden, pc->kv_elems);
+        const uint32_t bits =
+            (pi.clamp < 0 ? 1u : 0u) | (pi.clamp > 0 ? 2u : 0u) | cell.clamp_tw;
         if (bits) atomicOr(&clampbits[c], bits);
-      } else if (q < Qc + pc.K) {
-        const int k = q - Qc;
-        const int g = pc.k0 + k;
-        const double payload =
-            __dmul_rn(__dmul_rn(__ldg(p.P.coll_ppt + g), total_d), __ldg(p.P.coll_share + g));
-        int clamp;
-        sample_curve(p.S, __ldg(p.coll_tab + g), payload, t, en, clamp);
-        en = __dmul_rn(en, double(__ldg(p.P.coll_groups + g)));
-        if (clamp) atomicOr(&clampbits[pc.C + k], clamp < 0 ? 1u : 2u);
       } else {
-        const int b = q - Qc - pc.K;
-        const double payload = __dmul_rn(pc.p2p_ppt, total_d);
+        const int k = q - Qc;  // K collectives, then ND distinct p2p curves
+        const CurveConst& cu = cv[k];
+        const double payload = __dmul_rn(__dmul_rn(cu.ppt, total_d), cu.share);
         int clamp;
-        sample_curve(p.S, __ldg(p.p2p_tab + pc.b0 + b), payload, t, en, clamp);
-        if (clamp) atomicOr(&clampbits[pc.C + pc.K + b], clamp < 0 ? 1u : 2u);
+        sample_curve(cu, payload, t, en, clamp);
+        if (k < K) {
+          en = __dmul_rn(en, cu.emul);  // query_energy * groups_per_stage
+        } else {
+          p2p_val[k - K] = t;
+          p2p_val[kMaxClampSlots + k - K] = en;
+        }
+        if (clamp) atomicOr(&clampbits[C + k], clamp < 0 ? 1u : 2u);
       }
       qv[lane] = t;
       qv[kWarp + lane] = en;
@@ -126,41 +159,38 @@ __device__ void eval_iteration(const SimParams& p, const PlanConst& pc,
     }
     __syncwarp();
     const int here = min(kWarp, Q - base);
-    for (int l = 0; l < here; ++l) {
-      const int q2 = base + l;
-      const double t = qv[l], en = qv[kWarp + l];
-      if (q2 < Qc) {
-        bs = __dadd_rn(bs, t);
-        bj = __dadd_rn(bj, en);
-        bf = __dadd_rn(bf, qv[2 * kWarp + l]);
-        bb = __dadd_rn(bb, qv[3 * kWarp + l]);
-      } else if (q2 < Qc + pc.K) {
-        bs = __dadd_rn(bs, t);
-        bj = __dadd_rn(bj, en);
-      } else {
-        if (!staged) {
-          srep = __dmul_rn(bs, pc.reps);
-          jrep = __dmul_rn(bj, pc.reps);
-          d = dmax_ref(0.0, srep);
-          e = __dadd_rn(0.0, jrep);
-          staged = true;
-        }
-        d = dmax_ref(d, __dadd_rn(srep, t));
-        e = __dadd_rn(e, __dadd_rn(jrep, en));
-      }
+    const int cell_end = min(here, max(0, Qc - base));
+    const int coll_end = min(here, max(0, Qc + K - base));
+    int l = 0;
+    for (; l < cell_end; ++l) {
+      bs = __dadd_rn(bs, qv[l]);
+      bj = __dadd_rn(bj, qv[kWarp + l]);
+      bf = __dadd_rn(bf, qv[2 * kWarp + l]);
+      bb = __dadd_rn(bb, qv[3 * kWarp + l]);
+    }
+    for (; l < coll_end; ++l) {
+      bs = __dadd_rn(bs, qv[l]);
+      bj = __dadd_rn(bj, qv[kWarp + l]);
     }
     __syncwarp();
   }
-  if (!staged) {
-    srep = __dmul_rn(bs, pc.reps);
-    jrep = __dmul_rn(bj, pc.reps);
-    d = dmax_ref(0.0, srep);
-    e = __dadd_rn(0.0, jrep);
+  // ---- stages (simulator.cpp:64-78, :125-130): every stage prices the same
+  // block * reps; boundary b adds its p2p to stage b+1 ----
+  const double srep = __dmul_rn(bs, pc->reps);
+  const double jrep = __dmul_rn(bj, pc->reps);
+  double d = dmax_ref(0.0, srep);
+  double e = __dadd_rn(0.0, jrep);
+  for (int b = 0; b < pc->NB; ++b) {
+    const int s = p2p_slot[b];
+    d = dmax_ref(d, __dadd_rn(srep, p2p_val[s]));
+    e = __dadd_rn(e, __dadd_rn(jrep, p2p_val[kMaxClampSlots + s]));
   }
-  dur = d;
-  energy = e;
-  dflops = __dmul_rn(__dmul_rn(__dmul_rn(bf, pc.sdd), pc.reps), pc.Sd);
-  dbytes = __dmul_rn(__dmul_rn(__dmul_rn(bb, pc.sdd), pc.reps), pc.Sd);
+  Cost r;
+  r.dur = d;
+  r.energy = e;
+  r.flops = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), pc->reps), pc->Sd);
+  r.bytes = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), pc->reps), pc->Sd);
+  return r;
 }
 
 }  // namespace
@@ -169,18 +199,28 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   const int lane = threadIdx.x;
   const unsigned lt_mask = (1u << lane) - 1u;
   const Unit U = p.units[blockIdx.x];
+#ifdef PSG_PHASE_PROFILE
+  unsigned long long prof_acc[kProfSlots] = {};
+  const long long prof_start = clock64();
+#endif
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* qv = reinterpret_cast<double*>(smem_raw);                  // 4 x 32
-  CellConst* cc = reinterpret_cast<CellConst*>(qv + 4 * kWarp);       // kMaxCells
-  uint32_t* clampbits = reinterpret_cast<uint32_t*>(cc + kMaxCells);  // kMaxClampSlots
-  double* memo = reinterpret_cast<double*>(clampbits + kMaxClampSlots);  // memo_cap x 4
-  double* s_adm = memo + 4 * p.memo_cap;
-  double* s_ft = s_adm + p.smem_cap;
-  int64_t* s_fin = reinterpret_cast<int64_t*>(s_ft + p.smem_cap);
-  int32_t* s_i32 = reinterpret_cast<int32_t*>(s_fin + p.smem_cap);   // 5 x smem_cap
+  const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem);
+  double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
+  PlanConst* pcs = reinterpret_cast<PlanConst*>(smem_raw + L.pc);
+  CellConst* cc = reinterpret_cast<CellConst*>(smem_raw + L.cc);
+  CurveConst* cv = reinterpret_cast<CurveConst*>(smem_raw + L.cv);
+  uint8_t* p2p_slot = reinterpret_cast<uint8_t*>(smem_raw + L.p2p_slot);
+  double* p2p_val = reinterpret_cast<double*>(smem_raw + L.p2p_val);
+  int32_t* combo = reinterpret_cast<int32_t*>(smem_raw + L.combo);
+  uint32_t* clampbits = reinterpret_cast<uint32_t*>(smem_raw + L.clamp);
+  double* w_arr = reinterpret_cast<double*>(smem_raw + L.win_arr);
+  int32_t* w_i32 = reinterpret_cast<int32_t*>(smem_raw + L.win_i32);  // tidx, ctx, gen, slot
+  double* memo = reinterpret_cast<double*>(smem_raw + L.memo);
+  double* tab = p.tab_smem > 0 ? reinterpret_cast<double*>(smem_raw + L.tab)
+                               : p.g_tab + size_t(blockIdx.x) * size_t(p.tab_cap);
 
-  // ---- plan constants (warp-uniform) ----
+  // ---- plan constants (warp-uniform, also staged for the evaluator) ----
   const int pl = U.plan;
   PlanConst pc;
   pc.kv = p.P.kv[pl];
@@ -199,9 +239,29 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   pc.K = p.P.coll_begin[pl + 1] - pc.k0;
   pc.b0 = p.P.p2p_begin[pl];
   pc.NB = p.P.p2p_begin[pl + 1] - pc.b0;
-
+  // distinct p2p tables (boundaries only span 1 or 2 nodes in practice)
+  int ND = 0;
+  {
+    int dist_tab[kMaxClampSlots];
+    for (int b = 0; b < pc.NB; ++b) {
+      const int t = p.p2p_tab[pc.b0 + b];
+      int s = 0;
+      while (s < ND && dist_tab[s] != t) ++s;
+      if (s == ND) dist_tab[ND++] = t;
+      if (lane == 0) p2p_slot[b] = uint8_t(s);
+    }
+    pc.ND = ND;
+    for (int s = lane; s < ND; s += kWarp) {
+      CurveConst c;
+      c.table = dist_tab[s];
+      cv[pc.K + s] = c;
+    }
+  }
+  if (lane == 0) *pcs = pc;
   for (int s = lane; s < kMaxClampSlots; s += kWarp) clampbits[s] = 0;
   for (int i = lane; i < 4 * p.memo_cap; i += kWarp) memo[i] = -1.0;
+
+  // ---- stage the unit's tables ----
   if (lane < pc.C) {
     CellConst c;
     const int g = pc.c0 + lane;
@@ -210,39 +270,118 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     c.tasks = p.P.cell_tasks[g];
     c.width = p.P.cell_width[g];
     c.scale = p.P.cell_scale[g];
+    c.ncombo = 0;
+    c.clamp_tw = 0;
+    c.n_ctx = 1;
     if (c.table >= 0) {
       c.n_ctx = p.S.c_n_ctx[c.table];
-      c.n_tasks = p.S.c_n_tasks[c.table];
-      c.n_width = p.S.c_n_width[c.table];
-      c.knot_begin = p.S.c_knot_begin[c.table];
-      c.value_begin = p.S.c_value_begin[c.table];
-      c.pj = locate(p.S.c_knots + c.knot_begin + c.n_ctx, c.n_tasks, c.tasks);
-      c.pk = locate(p.S.c_knots + c.knot_begin + c.n_ctx + c.n_tasks, c.n_width, c.width);
-    } else {
-      c.n_ctx = c.n_tasks = c.n_width = 1;
-      c.knot_begin = c.value_begin = 0;
-      c.pj = c.pk = AxisPos{0, 0, 0.0, 0};
+      const int nt = p.S.c_n_tasks[c.table], nw = p.S.c_n_width[c.table];
+      const double* kn = p.S.c_knots + p.S.c_knot_begin[c.table];
+      const AxisPos pj = locate(kn + c.n_ctx, nt, c.tasks);
+      const AxisPos pk = locate(kn + c.n_ctx + nt, nw, c.width);
+      c.clamp_tw = uint32_t(pj.clamp < 0) << 2 | uint32_t(pj.clamp > 0) << 3 |
+                   uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
+      for (int cj = 0; cj < 2; ++cj) {
+        const double wj = cj ? pj.t : __dsub_rn(1.0, pj.t);
+        if (wj == 0.0) continue;
+        for (int ck = 0; ck < 2; ++ck) {
+          const double wk = ck ? pk.t : __dsub_rn(1.0, pk.t);
+          if (wk == 0.0) continue;
+          c.wj[c.ncombo] = wj;
+          c.wk[c.ncombo] = wk;
+          combo[lane * kMaxCombos + c.ncombo] = (cj ? pj.hi : pj.lo) * nw + (ck ? pk.hi : pk.lo);
+          ++c.ncombo;
+        }
+      }
     }
     cc[lane] = c;
   }
+  for (int k = lane; k < pc.K; k += kWarp) {
+    const int g = pc.k0 + k;
+    CurveConst c;
+    c.table = p.coll_tab[g];
+    c.ppt = p.P.coll_ppt[g];
+    c.share = p.P.coll_share[g];
+    c.emul = double(p.P.coll_groups[g]);
+    cv[k] = c;
+  }
+  for (int s = lane; s < ND; s += kWarp) {
+    cv[pc.K + s].ppt = pc.p2p_ppt;
+    cv[pc.K + s].share = 1.0;  // payload = p2p_ppt * tokens; x * 1.0 is exact
+    cv[pc.K + s].emul = 1.0;
+  }
+  __syncwarp();
+  {
+    size_t off = 0;
+    for (int c = 0; c < pc.C; ++c) {
+      const CellConst cl = cc[c];
+      double* kd = tab + off;
+      double* vd = kd + cl.n_ctx;
+      if (cl.table >= 0) {
+        const double* kn = p.S.c_knots + p.S.c_knot_begin[cl.table];
+        const double* vs = p.S.c_seconds + p.S.c_value_begin[cl.table];
+        const double* vj = p.S.c_joules + p.S.c_value_begin[cl.table];
+        const int plane = p.S.c_n_tasks[cl.table] * p.S.c_n_width[cl.table];
+        for (int i = lane; i < cl.n_ctx; i += kWarp) kd[i] = kn[i];
+        for (int i = lane; i < cl.n_ctx * cl.ncombo; i += kWarp) {
+          const int r = i / cl.ncombo, cb = i - r * cl.ncombo;
+          const int64_t v = int64_t(r) * plane + combo[c * kMaxCombos + cb];
+          vd[2 * i] = vs[v];
+          vd[2 * i + 1] = vj[v];
+        }
+      }
+      if (lane == 0) {
+        cc[c].knots = kd;
+        cc[c].vals = vd;
+      }
+      off += size_t(cl.n_ctx) * (1 + 2 * cl.ncombo);
+    }
+    for (int k = 0; k < pc.K + ND; ++k) {
+      const int t = cv[k].table;
+      const int n = t >= 0 ? p.S.k_n[t] : 1;
+      double* x = tab + off;
+      if (t >= 0) {
+        const int64_t b = p.S.k_begin[t];
+        for (int i = lane; i < n; i += kWarp) {
+          x[i] = p.S.k_payload[b + i];
+          x[n + i] = p.S.k_seconds[b + i];
+          x[2 * n + i] = p.S.k_joules[b + i];
+        }
+      }
+      if (lane == 0) {
+        cv[k].x = x;
+        cv[k].s = x + n;
+        cv[k].j = x + 2 * n;
+        cv[k].n = n;
+      }
+      off += 3 * size_t(n);
+    }
+  }
   __syncwarp();
 
-  // ---- active list storage ----
+  // ---- active list ----
   int cap_now = p.smem_cap;
   ActiveList a;
-  a.adm = s_adm;
-  a.ft = s_ft;
-  a.fin = s_fin;
-  a.tidx = s_i32;
-  a.ctx = s_i32 + p.smem_cap;
-  a.gen = s_i32 + 2 * p.smem_cap;
-  a.done = s_i32 + 3 * p.smem_cap;
-  a.items = s_i32 + 4 * p.smem_cap;
+  {
+    double* af = reinterpret_cast<double*>(smem_raw + L.act_f64);
+    int32_t* ai = reinterpret_cast<int32_t*>(smem_raw + L.act_i32);
+    const int sc = p.smem_cap;
+    a.adm = af;
+    a.ft = af + sc;
+    a.arr = af + 2 * sc;
+    a.fin = reinterpret_cast<int64_t*>(smem_raw + L.act_fin);
+    a.tidx = ai;
+    a.ctx = ai + sc;
+    a.gen = ai + 2 * sc;
+    a.done = ai + 3 * sc;
+    a.slot = ai + 4 * sc;
+    a.items = ai + 5 * sc;
+  }
   const size_t nr = size_t(U.n_req);
-  int32_t* g_stack = p.g_i32 + size_t(U.scratch) * 6;  // 6 int32 arrays of n_req
-  double* g_f = p.g_f64 + size_t(U.scratch) * 3;      // adm, ft, fin(int64)
+  int32_t* g_i = p.g_i32 + size_t(U.scratch) * kGI32;  // [stack | tidx ctx gen done slot items]
+  double* g_f = p.g_f64 + size_t(U.scratch) * kGF64;   // [adm | ft | arr | fin]
+  int32_t* g_stack = g_i;
 
-  // ---- replica request sequence (round-robin split, simulator.cpp:187-193) ----
   auto req_tidx = [&](int j) -> int {
     return p.T.seq ? p.T.seq[U.seq_base + j]
                    : int(int64_t(U.replica) + int64_t(j) * U.replicas);
@@ -258,30 +397,119 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
 
   double clock = 0.0, energy = 0.0, flops = 0.0, bytes = 0.0;
   int64_t n = 0, max_batch = 0, completed = 0, rejected = 0, sum_batch = 0, admissions = 0;
-  int B = 0, n_pre = 0, pend = 0, stack_top = 0;
-  int64_t used = 0;          // KV ledger in tokens: sum(ctx + generated)
+  int pend = 0, stack_top = 0, w_base = -kWindow;
+  // Active slots in admission order with tombstones: B live of len used,
+  // live slots below first_pre are all decode-phase (prefill frontier).
+  int B = 0, len = 0, first_pre = 0, n_pre = 0;
+  int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated)
   int64_t next_fin = kNoFin;
   int err = 0;
 
+  // pending head (batching.hpp:93 pending_.front()), warp-uniform registers
+  bool hd_valid = false, hd_stack = false;
+  double hd_arr = 0.0;
+  int hd_tidx = 0, hd_ctx = 0, hd_gen = 0, hd_slot = 0;
+  auto load_head = [&]() {
+    if (stack_top > 0) {  // evicted requests re-enter at the queue head
+      hd_tidx = g_stack[stack_top - 1];
+      hd_arr = p.T.arrival[hd_tidx];
+      hd_ctx = int(p.T.ctx[hd_tidx]);
+      hd_gen = int(p.T.gen[hd_tidx]);
+      hd_slot = p.T.slot[hd_tidx];
+      hd_valid = hd_stack = true;
+      return;
+    }
+    hd_stack = false;
+    hd_valid = pend < U.n_req;
+    if (!hd_valid) return;
+    if (pend >= w_base + kWindow) {  // refill the prefetch window
+      PROF_T0(t_ref);
+      w_base = pend;
+      const int j = w_base + lane;
+      if (j < U.n_req) {
+        const int t = req_tidx(j);
+        w_arr[lane] = p.T.arrival[t];
+        w_i32[lane] = t;
+        w_i32[kWindow + lane] = int(p.T.ctx[t]);
+        w_i32[2 * kWindow + lane] = int(p.T.gen[t]);
+        w_i32[3 * kWindow + lane] = p.T.slot[t];
+      }
+      __syncwarp();
+      PROF_ADD(9, t_ref);
+    }
+    const int w = pend - w_base;
+    hd_arr = w_arr[w];
+    hd_tidx = w_i32[w];
+    hd_ctx = w_i32[kWindow + w];
+    hd_gen = w_i32[2 * kWindow + w];
+    hd_slot = w_i32[3 * kWindow + w];
+  };
   auto fits = [&](int64_t tokens) -> bool {  // double(tokens) * kv <= cap, exact
     return !(__dmul_rn(double(tokens), kv) > cap);
   };
-  auto reject_slot = [&](int tidx) {
-    if (lane == 0) p.slot_status[slot_base + p.T.slot[tidx]] = 2;
+  auto reject_slot = [&](int slot) {
+    if (lane == 0) p.slot_status[slot_base + slot] = 2;
     ++rejected;
   };
+  auto min_rel = [&](int64_t fin, int64_t base) -> unsigned {  // decode slots only
+    return (fin == kNoFin || fin == kDead) ? kNoRel : unsigned(fin - base);
+  };
+  // Order-preserving in-place compaction of the live slots.
+  auto compact = [&]() {
+    __syncwarp();
+    int w = 0, below = 0;
+    for (int base = 0; base < len; base += kWarp) {
+      const int i = base + lane;
+      const int64_t fin = i < len ? a.fin[i] : kDead;
+      const bool live = fin != kDead;
+      int32_t tidx = 0, ctx = 0, gen = 0, done = 0, slot = 0;
+      double adm = 0.0, ft = 0.0, arr = 0.0;
+      if (live) {
+        tidx = a.tidx[i];
+        ctx = a.ctx[i];
+        gen = a.gen[i];
+        done = a.done[i];
+        slot = a.slot[i];
+        adm = a.adm[i];
+        ft = a.ft[i];
+        arr = a.arr[i];
+      }
+      const unsigned km = __ballot_sync(kFull, live);
+      const int pos = w + __popc(km & lt_mask);
+      below += __popc(__ballot_sync(kFull, live && i < first_pre));
+      __syncwarp();
+      if (live) {
+        a.tidx[pos] = tidx;
+        a.ctx[pos] = ctx;
+        a.gen[pos] = gen;
+        a.done[pos] = done;
+        a.slot[pos] = slot;
+        a.fin[pos] = fin;
+        a.adm[pos] = adm;
+        a.ft[pos] = ft;
+        a.arr[pos] = arr;
+      }
+      w += __popc(km);
+      __syncwarp();
+    }
+    len = w;
+    first_pre = below;
+  };
   auto migrate = [&]() {
-    // Move the active list (and prefill-item scratch) to the unit's global
-    // region; capacity becomes n_req, the largest possible batch.
-    int32_t* gi = g_stack + nr;
-    int64_t* gfin = reinterpret_cast<int64_t*>(g_f + 2 * nr);
-    for (int i = lane; i < B; i += kWarp) {
+    // Move the active slots to the unit's global region: capacity n_req.
+    if (len > B) compact();
+    __syncwarp();
+    int32_t* gi = g_i + nr;
+    int64_t* gfin = reinterpret_cast<int64_t*>(g_f + 3 * nr);
+    for (int i = lane; i < len; i += kWarp) {
       gi[i] = a.tidx[i];
       gi[nr + i] = a.ctx[i];
       gi[2 * nr + i] = a.gen[i];
       gi[3 * nr + i] = a.done[i];
+      gi[4 * nr + i] = a.slot[i];
       g_f[i] = a.adm[i];
       g_f[nr + i] = a.ft[i];
+      g_f[2 * nr + i] = a.arr[i];
       gfin[i] = a.fin[i];
     }
     __syncwarp();
@@ -289,316 +517,341 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     a.ctx = gi + nr;
     a.gen = gi + 2 * nr;
     a.done = gi + 3 * nr;
-    a.items = gi + 4 * nr;
+    a.slot = gi + 4 * nr;
+    a.items = gi + 5 * nr;
     a.adm = g_f;
     a.ft = g_f + nr;
+    a.arr = g_f + 2 * nr;
     a.fin = gfin;
     cap_now = int(nr);
   };
-  auto recompute_next_fin = [&]() {
-    int64_t m = kNoFin;
-    for (int base = 0; base < B; base += kWarp) {
+  // Drops trailing tombstones so slot len-1 is the newest live request.
+  auto trim = [&]() {
+    __syncwarp();
+    while (len > 0) {
+      const int base = len > kWarp ? len - kWarp : 0;
       const int i = base + lane;
-      const int64_t f = i < B ? a.fin[i] : kNoFin;
-      m = f < m ? f : m;
+      const unsigned lm = __ballot_sync(kFull, i < len && a.fin[i] != kDead);
+      if (lm) {
+        len = base + kWarp - __clz(lm);
+        break;
+      }
+      len = base;
     }
-    next_fin = warp_min_i64(m);
+    first_pre = first_pre < len ? first_pre : len;
+  };
+  auto recompute_next_fin = [&]() {
+    unsigned m = kNoRel;
+    for (int base = 0; base < len; base += kWarp) {
+      const int i = base + lane;
+      m = min(m, __reduce_min_sync(kFull, i < len ? min_rel(a.fin[i], n) : kNoRel));
+    }
+    next_fin = m == kNoRel ? kNoFin : n + m;
   };
   // Finish removal (batching.cpp:95-102) + metrics (simulator.cpp:143-156),
-  // then LIFO eviction (batching.cpp:110-125).  Runs at iteration n, after
-  // the clock has advanced.
+  // then LIFO eviction (batching.cpp:110-125), at iteration n after the clock
+  // has advanced.  Finished slots become tombstones.
   auto finish_and_evict = [&]() {
+    PROF_T0(t_fin);
     if (next_fin == n) {
-      int w = 0;
-      int64_t freed = 0, m = kNoFin, nfin = 0;
-      for (int base = 0; base < B; base += kWarp) {
+      PROF_CNT(13);
+      int64_t freed = 0;
+      unsigned m = kNoRel, nfin = 0;
+      for (int base = 0; base < len; base += kWarp) {
         const int i = base + lane;
-        const bool valid = i < B;
-        int32_t tidx = 0, ctx = 0, gen = 0, done = 0;
-        int64_t fin = kNoFin;
-        double adm = 0.0, ft = 0.0;
-        if (valid) {
-          tidx = a.tidx[i];
-          ctx = a.ctx[i];
-          gen = a.gen[i];
-          done = a.done[i];
-          fin = a.fin[i];
-          adm = a.adm[i];
-          ft = a.ft[i];
-        }
-        const bool fnow = valid && fin == n;
+        const int64_t fin = i < len ? a.fin[i] : kDead;
+        const bool fnow = fin == n;
+        unsigned tok = 0;
         if (fnow) {
-          const double arr = p.T.arrival[tidx];
-          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : adm;
-          const size_t s = slot_base + p.T.slot[tidx];
+          const int32_t gen = a.gen[i];
+          const double arr = a.arr[i], ft = a.ft[i];
+          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
+          const size_t s = slot_base + a.slot[i];
           p.slot_e2e[s] = __dsub_rn(clock, arr);
           p.slot_ttft[s] = __dsub_rn(ft, anchor);
-          p.slot_tpot[s] =
-              gen >= 2 ? __ddiv_rn(__dsub_rn(clock, ft), double(gen - 1)) : 0.0;
+          p.slot_tpot[s] = gen >= 2 ? __ddiv_rn(__dsub_rn(clock, ft), double(gen - 1)) : 0.0;
           p.slot_status[s] = 1;
+          a.fin[i] = kDead;
+          tok = unsigned(a.ctx[i] + gen);
         }
-        const bool keep = valid && !fnow;
-        const unsigned km = __ballot_sync(kFull, keep);
-        const int pos = w + __popc(km & lt_mask);
-        __syncwarp();
-        if (keep) {
-          a.tidx[pos] = tidx;
-          a.ctx[pos] = ctx;
-          a.gen[pos] = gen;
-          a.done[pos] = done;
-          a.fin[pos] = fin;
-          a.adm[pos] = adm;
-          a.ft[pos] = ft;
-        }
-        w += __popc(km);
-        freed += warp_sum_i64(fnow ? int64_t(ctx) + gen : 0);
+        freed += int64_t(__reduce_add_sync(kFull, tok));
         nfin += __popc(__ballot_sync(kFull, fnow));
-        const int64_t fk = keep ? fin : kNoFin;
-        m = fk < m ? fk : m;
-        __syncwarp();
+        m = min(m, __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n)));
       }
-      B = w;
-      used -= freed;
+      B -= int(nfin);
       completed += nfin;
-      next_fin = warp_min_i64(m);
+      used -= freed;
+      next_fin = m == kNoRel ? kNoFin : n + m;
+      trim();
+      if (len > 2 * B + 2 * kWarp) compact();
     }
+    PROF_ADD(7, t_fin);
+    PROF_T0(t_ev);
     bool evicted = false;
     while (B > 1 && !fits(used)) {
-      const int i = B - 1;
+      const int i = len - 1;  // newest live request (trim invariant)
       const int64_t fin = a.fin[i];
-      const int32_t ctx = a.ctx[i], gen = a.gen[i];
-      const int64_t tok = fin == kNoFin ? 0 : int64_t(gen) - (fin - n);
-      used -= int64_t(ctx) + tok;
+      const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
+      used -= int64_t(a.ctx[i]) + tok;
       if (fin == kNoFin) --n_pre;
-      if (lane == 0) g_stack[stack_top] = a.tidx[i];  // push_front of pending
+      if (lane == 0) {
+        g_stack[stack_top] = a.tidx[i];  // push_front of pending
+        a.fin[i] = kDead;
+      }
       ++stack_top;
       --B;
       evicted = true;
+      trim();
     }
     if (B == 1 && !fits(used)) {
-      reject_slot(a.tidx[0]);
-      B = 0;
-      n_pre = 0;
+      reject_slot(a.slot[len - 1]);
+      B = len = first_pre = n_pre = 0;
       used = 0;
       next_fin = kNoFin;
       evicted = false;
     }
     __syncwarp();
-    if (evicted) recompute_next_fin();
+    if (evicted) {
+      load_head();
+      recompute_next_fin();
+    }
+    PROF_ADD(8, t_ev);
   };
 
+  load_head();
   while (true) {
     // ---- admit (batching.cpp:35-60) ----
-    while (true) {
-      int h;
-      if (stack_top > 0) h = g_stack[stack_top - 1];
-      else if (pend < U.n_req) h = req_tidx(pend);
-      else break;
-      if (!(p.T.arrival[h] <= clock)) break;
-      const int64_t ctx = p.T.ctx[h];
-      if (__dmul_rn(double(ctx), kv) > cap) {
-        reject_slot(h);
-        if (stack_top > 0) --stack_top; else ++pend;
-        continue;
+    PROF_T0(t_adm);
+    while (hd_valid && hd_arr <= clock) {
+      const bool reject = __dmul_rn(double(hd_ctx), kv) > cap;
+      if (!reject) {
+        if (max_bs > 0 && int64_t(B) >= max_bs) break;
+        if (!fits(used + hd_ctx)) break;
+        if (len >= cap_now) {
+          if (len > B) compact();
+          if (len >= cap_now) migrate();
+        }
+        if (lane == 0) {
+          a.tidx[len] = hd_tidx;
+          a.ctx[len] = hd_ctx;
+          a.gen[len] = hd_gen;
+          a.done[len] = 0;
+          a.slot[len] = hd_slot;
+          a.fin[len] = kNoFin;
+          a.adm[len] = clock;
+          a.ft[len] = 0.0;
+          a.arr[len] = hd_arr;
+        }
+        ++len;
+        ++B;
+        ++n_pre;
+        ++admissions;
+        used += hd_ctx;
+      } else {
+        reject_slot(hd_slot);
       }
-      if (max_bs > 0 && int64_t(B) >= max_bs) break;
-      if (!fits(used + ctx)) break;
-      if (B >= cap_now) migrate();
-      if (lane == 0) {
-        a.tidx[B] = h;
-        a.ctx[B] = int32_t(ctx);
-        a.gen[B] = int32_t(p.T.gen[h]);
-        a.done[B] = 0;
-        a.fin[B] = kNoFin;
-        a.adm[B] = clock;
-        a.ft[B] = 0.0;
-      }
-      ++B;
-      ++n_pre;
-      ++admissions;
-      used += ctx;
-      if (stack_top > 0) --stack_top; else ++pend;
+      if (hd_stack) --stack_top; else ++pend;
+      load_head();
     }
     __syncwarp();
+    PROF_ADD(0, t_adm);
 
     if (B == 0) {  // idle (simulator.cpp:116-120)
-      int h;
-      if (stack_top > 0) h = g_stack[stack_top - 1];
-      else if (pend < U.n_req) h = req_tidx(pend);
-      else break;
-      clock = dmax_ref(clock, p.T.arrival[h]);
+      if (!hd_valid) break;
+      clock = dmax_ref(clock, hd_arr);
       continue;
     }
     if (chunk_err) { err = 1; break; }
     if (missing) { err = 2; break; }
 
+    bool settle = true;
     if (n_pre > 0) {
-      // ---- mixed iteration: literal step (batching.cpp:62-108) ----
+      // ---- mixed iteration: literal step (batching.cpp:62-108) over the
+      // prefill frontier only ----
+      PROF_CNT(10);
+      PROF_T0(t_m1);
       int n_items = 0;
       int64_t pre_tok = 0;
-      for (int base = 0; base < B; base += kWarp) {
+      for (int base = first_pre; base < len; base += kWarp) {
         const int i = base + lane;
-        bool pre = false;
-        int64_t tok = 0;
-        if (i < B && a.fin[i] == kNoFin) {
-          pre = true;
-          tok = int64_t(a.ctx[i]) - a.done[i];
-          if (chunked) tok = tok < chunk ? tok : chunk;
+        const bool pre = i < len && a.fin[i] == kNoFin;
+        int tok = 0;
+        if (pre) {
+          int64_t t = int64_t(a.ctx[i]) - a.done[i];
+          if (chunked) t = t < chunk ? t : chunk;
+          tok = int(t);
         }
         const unsigned pm = __ballot_sync(kFull, pre);
-        if (pre) a.items[n_items + __popc(pm & lt_mask)] = int32_t(tok);
+        if (pre) a.items[n_items + __popc(pm & lt_mask)] = tok;
         n_items += __popc(pm);
-        pre_tok += warp_sum_i64(tok);
+        pre_tok += __reduce_add_sync(kFull, unsigned(tok));
       }
       __syncwarp();
       const int64_t decode = int64_t(B) - n_items;
-      double d, e, f, b;
-      eval_iteration(p, pc, cc, a.items, n_items, decode, decode + pre_tok, qv,
-                     clampbits, d, e, f, b);
-      clock = __dadd_rn(clock, d);
-      energy = __dadd_rn(energy, e);
-      flops = __dadd_rn(flops, f);
-      bytes = __dadd_rn(bytes, b);
+      PROF_ADD(1, t_m1);
+      PROF_T0(t_m2);
+      const Cost c = eval_iteration(pcs, cc, cv, p2p_slot, p2p_val, a.items, n_items, decode,
+                                    decode + pre_tok, qv, clampbits);
+      PROF_ADD(2, t_m2);
+      PROF_T0(t_m3);
+      clock = __dadd_rn(clock, c.dur);
+      energy = __dadd_rn(energy, c.energy);
+      flops = __dadd_rn(flops, c.flops);
+      bytes = __dadd_rn(bytes, c.bytes);
       max_batch = max_batch > B ? max_batch : int64_t(B);
       sum_batch += B;
       const int64_t n_new = n + 1;
-      int64_t ncompl = 0, m = next_fin;
-      for (int base = 0; base < B; base += kWarp) {
+      unsigned ncompl = 0, m = min_rel(next_fin, n_new);
+      int new_fp = -1;
+      for (int base = first_pre; base < len; base += kWarp) {
         const int i = base + lane;
-        bool compl_now = false;
-        int64_t fin = kNoFin;
-        if (i < B && a.fin[i] == kNoFin) {
+        bool compl_now = false, still = false;
+        unsigned rel = kNoRel;
+        if (i < len && a.fin[i] == kNoFin) {
           const int32_t ctx = a.ctx[i];
           int64_t tok = int64_t(ctx) - a.done[i];
           if (chunked) tok = tok < chunk ? tok : chunk;
           const int64_t done = a.done[i] + tok;
           a.done[i] = int32_t(done);
-          if (done == ctx) {  // prefill iteration samples the first token
+          if (done == ctx) {  // the prefill iteration samples the first token
             const int32_t gen = a.gen[i];
-            fin = n_new + (gen > 1 ? gen - 1 : 0);
+            const int64_t fin = n_new + (gen > 1 ? gen - 1 : 0);
             a.fin[i] = fin;
             a.ft[i] = clock;
             compl_now = true;
+            rel = unsigned(fin - n_new);
+          } else {
+            still = true;
           }
         }
         ncompl += __popc(__ballot_sync(kFull, compl_now));
-        const int64_t wm = warp_min_i64(fin);
-        m = wm < m ? wm : m;
+        m = min(m, __reduce_min_sync(kFull, rel));
+        const unsigned sm = __ballot_sync(kFull, still);
+        if (new_fp < 0 && sm) new_fp = base + __ffs(sm) - 1;
       }
       __syncwarp();
-      used += decode + ncompl;
+      first_pre = new_fp < 0 ? len : new_fp;
+      used += decode + int64_t(ncompl);
       n_pre -= int(ncompl);
       n = n_new;
-      next_fin = m;
-      finish_and_evict();
-      continue;
-    }
-
-    // ---- decode-only run: exact macro-stepping ----
-    double d, e, f, b;
-    if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
-      d = memo[4 * (B - 1)];
-      e = memo[4 * (B - 1) + 1];
-      f = memo[4 * (B - 1) + 2];
-      b = memo[4 * (B - 1) + 3];
+      next_fin = m == kNoRel ? kNoFin : n + m;
+      PROF_ADD(3, t_m3);
     } else {
-      eval_iteration(p, pc, cc, a.items, 0, B, B, qv, clampbits, d, e, f, b);
-      if (B <= p.memo_cap) {
-        __syncwarp();
-        if (lane == 0) {
-          memo[4 * (B - 1) + 1] = e;
-          memo[4 * (B - 1) + 2] = f;
-          memo[4 * (B - 1) + 3] = b;
-          memo[4 * (B - 1)] = d;
+      PROF_CNT(11);
+      PROF_T0(t_d1);
+      // ---- decode-only run: exact macro-stepping ----
+      Cost c;
+      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
+        c.dur = memo[4 * (B - 1)];
+        c.energy = memo[4 * (B - 1) + 1];
+        c.flops = memo[4 * (B - 1) + 2];
+        c.bytes = memo[4 * (B - 1) + 3];
+      } else {
+        PROF_CNT(12);
+        c = eval_iteration(pcs, cc, cv, p2p_slot, p2p_val, a.items, 0, B, B, qv, clampbits);
+        if (B <= p.memo_cap) {
+          if (lane == 0) {
+            memo[4 * (B - 1) + 1] = c.energy;
+            memo[4 * (B - 1) + 2] = c.flops;
+            memo[4 * (B - 1) + 3] = c.bytes;
+            memo[4 * (B - 1)] = c.dur;
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
-    }
-    // k_fin: iterations until the first finish (inclusive).
-    int64_t kmax = next_fin - n;
-    // k_ovf: first k with (used + k*B)*kv > cap.
-    if (!fits(used + kmax * int64_t(B))) {
-      const double r = (cap / kv - double(used)) / double(B);
-      int64_t k0 = r >= double(kmax) ? kmax - 1 : (r < 0.0 ? 0 : int64_t(floor(r)));
-      while (k0 > 0 && !fits(used + k0 * int64_t(B))) --k0;
-      while (k0 + 1 < kmax && fits(used + (k0 + 1) * int64_t(B))) ++k0;
-      kmax = k0 + 1;
-    }
-    // Arrival event: only a not-yet-arrived head can change the batch; an
-    // arrived head that the admit loop left in place is blocked for the
-    // whole run (used only grows, B is fixed).
-    bool check = false, rej_h = false;
-    double a_h = 0.0;
-    int64_t j_adm = -1;
-    if (stack_top == 0 && pend < U.n_req) {
-      const int h = req_tidx(pend);
-      a_h = p.T.arrival[h];
-      if (a_h > clock) {
-        const int64_t ctx_h = p.T.ctx[h];
-        rej_h = __dmul_rn(double(ctx_h), kv) > cap;
+      const double d = c.dur, e = c.energy, f = c.flops, b = c.bytes;
+      PROF_ADD(4, t_d1);
+      PROF_T0(t_d2);
+      // iterations until the first finish (inclusive)
+      int64_t kmax = next_fin - n;
+      // first k with (used + k*B)*kv > cap (batching.cpp:112 overflow)
+      if (!fits(used + kmax * int64_t(B))) {
+        const double r = (cap / kv - double(used)) / double(B);
+        int64_t k0 = r >= double(kmax) ? kmax - 1 : (r < 0.0 ? 0 : int64_t(floor(r)));
+        while (k0 > 0 && !fits(used + k0 * int64_t(B))) --k0;
+        while (k0 + 1 < kmax && fits(used + (k0 + 1) * int64_t(B))) ++k0;
+        kmax = k0 + 1;
+      }
+      // Arrival event: only a not-yet-arrived head can change the batch; an
+      // arrived head that admit() left in place stays blocked for the whole
+      // run (used only grows, B is fixed).
+      bool check = false, rej_h = false;
+      int64_t j_adm = -1;
+      if (hd_valid && !hd_stack && hd_arr > clock) {
+        rej_h = __dmul_rn(double(hd_ctx), kv) > cap;
         if (rej_h) {
           check = true;
-        } else if (!(max_bs > 0 && int64_t(B) >= max_bs) && fits(used + ctx_h)) {
+        } else if (!(max_bs > 0 && int64_t(B) >= max_bs) && fits(used + hd_ctx)) {
           check = true;
-          // largest j in [0, kmax] with used + j*B + ctx_h fitting
-          if (fits(used + kmax * int64_t(B) + ctx_h)) {
+          // largest j in [0, kmax] with used + j*B + ctx fitting
+          if (fits(used + kmax * int64_t(B) + hd_ctx)) {
             j_adm = kmax;
           } else {
-            const double r = (cap / kv - double(used + ctx_h)) / double(B);
+            const double r = (cap / kv - double(used + hd_ctx)) / double(B);
             int64_t j0 = r >= double(kmax) ? kmax - 1 : (r < 0.0 ? 0 : int64_t(floor(r)));
-            while (j0 > 0 && !fits(used + j0 * int64_t(B) + ctx_h)) --j0;
-            while (j0 + 1 < kmax && fits(used + (j0 + 1) * int64_t(B) + ctx_h)) ++j0;
+            while (j0 > 0 && !fits(used + j0 * int64_t(B) + hd_ctx)) --j0;
+            while (j0 + 1 < kmax && fits(used + (j0 + 1) * int64_t(B) + hd_ctx)) ++j0;
             j_adm = j0;
           }
         }
       }
+      int64_t j = 0;
+      bool stop = false;
+      PROF_ADD(5, t_d2);
+      PROF_T0(t_d3);
+      if (check) {
+        const double a_h = hd_arr;
+        while (j + 4 <= kmax) {
+          const double c1 = __dadd_rn(clock, d);
+          const double c2 = __dadd_rn(c1, d);
+          const double c3 = __dadd_rn(c2, d);
+          if (!(clock < a_h && c1 < a_h && c2 < a_h && c3 < a_h)) break;
+          clock = __dadd_rn(c3, d);
+          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+          j += 4;
+        }
+        while (j < kmax && clock < a_h) {
+          clock = __dadd_rn(clock, d);
+          energy = __dadd_rn(energy, e);
+          flops = __dadd_rn(flops, f);
+          bytes = __dadd_rn(bytes, b);
+          ++j;
+        }
+        if (j < kmax && (rej_h || j <= j_adm)) stop = true;
+      }
+      if (!stop) {
+        for (; j + 4 <= kmax; j += 4) {
+          clock = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(clock, d), d), d), d);
+          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+        }
+        for (; j < kmax; ++j) {
+          clock = __dadd_rn(clock, d);
+          energy = __dadd_rn(energy, e);
+          flops = __dadd_rn(flops, f);
+          bytes = __dadd_rn(bytes, b);
+        }
+      }
+      PROF_ADD(6, t_d3);
+      n += j;
+      used += j * int64_t(B);
+      sum_batch += j * int64_t(B);
+      if (j > 0) max_batch = max_batch > B ? max_batch : int64_t(B);
+      settle = !stop;
     }
-    int64_t j = 0;
-    bool stop = false;
-    if (check) {
-      while (j + 4 <= kmax) {
-        const double c1 = __dadd_rn(clock, d);
-        const double c2 = __dadd_rn(c1, d);
-        const double c3 = __dadd_rn(c2, d);
-        if (!(clock < a_h && c1 < a_h && c2 < a_h && c3 < a_h)) break;
-        clock = __dadd_rn(c3, d);
-        energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-        flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-        bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-        j += 4;
-      }
-      while (j < kmax && clock < a_h) {
-        clock = __dadd_rn(clock, d);
-        energy = __dadd_rn(energy, e);
-        flops = __dadd_rn(flops, f);
-        bytes = __dadd_rn(bytes, b);
-        ++j;
-      }
-      if (j < kmax && (rej_h || j <= j_adm)) stop = true;
-    }
-    if (!stop) {
-      for (; j + 4 <= kmax; j += 4) {
-        clock = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(clock, d), d), d), d);
-        energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-        flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-        bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-      }
-      for (; j < kmax; ++j) {
-        clock = __dadd_rn(clock, d);
-        energy = __dadd_rn(energy, e);
-        flops = __dadd_rn(flops, f);
-        bytes = __dadd_rn(bytes, b);
-      }
-    }
-    n += j;
-    used += j * int64_t(B);
-    sum_batch += j * int64_t(B);
-    if (j > 0) max_batch = max_batch > B ? max_batch : int64_t(B);
-    if (!stop) finish_and_evict();
+    if (settle) finish_and_evict();
   }
 
   // ---- unit outputs ----
   __syncwarp();
+#ifdef PSG_PHASE_PROFILE
+  prof_acc[15] = (unsigned long long)(clock64() - prof_start);
+  if (lane == 0 && p.prof)
+    for (int k = 0; k < kProfSlots; ++k) p.prof[size_t(blockIdx.x) * kProfSlots + k] = prof_acc[k];
+#endif
   if (lane == 0) {
     UnitOut o;
     o.clock = clock;
@@ -615,24 +868,26 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     o.pad = 0;
     p.uout[blockIdx.x] = o;
   }
-  const int nslots = pc.C + pc.K + pc.NB;
+  const int nslots = pc.C + pc.K + ND;
   for (int s = lane; s < nslots && s < kMaxClampSlots; s += kWarp) {
     const uint32_t bits = clampbits[s];
     if (!bits) continue;
-    if (s < pc.C) {
-      if (cc[s].table >= 0) atomicOr(p.clamp_compute + cc[s].table, bits);
-    } else if (s < pc.C + pc.K) {
-      atomicOr(p.clamp_curve + p.coll_tab[pc.k0 + s - pc.C], bits);
-    } else {
-      atomicOr(p.clamp_curve + p.p2p_tab[pc.b0 + s - pc.C - pc.K], bits);
-    }
+    const int t = s < pc.C ? cc[s].table : cv[s - pc.C].table;
+    if (t < 0) continue;
+    atomicOr((s < pc.C ? p.clamp_compute : p.clamp_curve) + t, bits);
   }
 }
 
-size_t sim_smem_bytes(int smem_cap, int memo_cap) {
-  return sizeof(double) * 4 * kWarp + sizeof(CellConst) * kMaxCells +
-         sizeof(uint32_t) * kMaxClampSlots + sizeof(double) * 4 * size_t(memo_cap) +
-         size_t(smem_cap) * (2 * sizeof(double) + sizeof(int64_t) + 5 * sizeof(int32_t));
+size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem) {
+  return smem_layout(smem_cap, memo_cap, tab_smem).total;
+}
+
+// Doubles of table staging a unit of this plan needs at most (host side).
+size_t sim_tab_doubles(int n_cells, const int* n_ctx, int n_curves, const int* curve_n) {
+  size_t t = 0;
+  for (int c = 0; c < n_cells; ++c) t += size_t(n_ctx[c]) * (1 + 2 * kMaxCombos);
+  for (int k = 0; k < n_curves; ++k) t += 3 * size_t(curve_n[k]);
+  return t;
 }
 
 }  // namespace psg

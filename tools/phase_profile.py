@@ -1,0 +1,53 @@
+"""Dev tool: per-phase cycle breakdown of the longest simulation units.
+
+    PSG_LIBRARY=libpsg_prof.so python tools/phase_profile.py c2 [--top 5]
+
+Runs one search on reference-dumped inputs with the profiler build and
+prints, for the critical units, where their cycles go (slots documented in
+psg_sim.cu).
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+sys.path.insert(0, os.path.join(REPO, "tests"))
+
+NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
+         "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "-", "total"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("key")
+    ap.add_argument("--top", type=int, default=5)
+    ap.add_argument("--workdir", default="/tmp/psg_probe")
+    args = ap.parse_args()
+    os.environ.setdefault("PSG_LIBRARY", "libpsg_prof.so")
+    out = os.path.join(args.workdir, f"phase_{args.key}.bin")
+    os.makedirs(args.workdir, exist_ok=True)
+    os.environ["PSG_PHASE_PROFILE"] = out
+    from harness import RefCase
+    from paper_2411_17651_b200.engine import Engine
+    case = RefCase(args.key, args.workdir)
+    eng = Engine(0)
+    res = eng.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 18)
+    meta, cnt = raw[:, :2].view(np.int64), raw[:, 2:]
+    order = np.argsort(-cnt[:, 15].astype(np.float64))
+    F = max(1, len(case.workload.freqs))
+    print(f"{args.key}: sim {res.ms['sim']:.2f} ms, units {len(raw)}")
+    for u in order[:args.top]:
+        tot = float(cnt[u, 15])
+        enc = case.plans.encodings[int(meta[u, 0]) // F]
+        parts = " ".join(f"{NAMES[k]}={100 * cnt[u, k] / tot:.1f}%" for k in range(10))
+        counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 14))
+        print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
+
+
+if __name__ == "__main__":
+    main()
