@@ -150,38 +150,73 @@ __device__ __forceinline__ AxisPos locate(const double* k, int n, double x) {
   return p;
 }
 
+// locate() with a segment hint (the segment of the table's previous query):
+// consecutive queries of one table mostly land in the same knot interval
+// (decode counts move by +-1 between events, payload knots are far apart), so
+// two loads and compares replace the binary search.  The hinted interval
+// k[h] <= x < k[h+1] gives exactly locate()'s (lo, hi, t), except x == k[0],
+// where it yields (0, 1, t = 0) instead of (0, 0, 0) — the same sample, as the
+// t-weighted corner then contributes an exact +0 (see sample()).
+__device__ __forceinline__ AxisPos locate_hint(const double* k, int n, double x, int h) {
+  if (h >= 0 && h + 1 < n) {
+    const double klo = k[h], khi = k[h + 1];
+    if (klo <= x && x < khi) {
+      AxisPos p;
+      p.lo = h;
+      p.hi = h + 1;
+      p.t = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(khi, klo));
+      p.clamp = 0;
+      return p;
+    }
+  }
+  return locate(k, n, x);
+}
+
 constexpr int kMaxCombos = 4;  // nonzero (tasks, width) corner pairs of a cell
 
-// A compute grid collapsed for one cell: the (tasks, width) coordinates are
-// fixed per (plan, cell), so only the context axis varies per query.  The
-// nonzero (cj, ck) corners are kept in the reference's loop order with their
-// weights, and their values are gathered into vals[n_ctx][ncombo][2]
-// (seconds, joules interleaved).
-struct CellConst {
-  int table;          // compute grid index (-1: missing)
-  int op;
-  int n_ctx, ncombo;
-  const double* knots;  // ctx knots
-  const double* vals;   // [n_ctx][ncombo][2]
+// One cost table as the evaluator sees it, in shared memory: knots[n] on the
+// queried axis and vals[n][ncombo][2] (seconds, joules interleaved).
+//  * compute grid of a cell: the (tasks, width) coordinates are fixed per
+//    (plan, cell), so the grid is collapsed to the context axis; the nonzero
+//    (cj, ck) corners are kept in the reference's loop order with weights
+//    wj, wk (cost.cpp:214-234);
+//  * collective curve: ncombo = 1, wj = wk = 1.  The generic sample
+//    0 + ((w*1)*1)*s_lo + ((t*1)*1)*s_hi then equals the reference's
+//    (1-t)*s[lo] + t*s[hi] (cost.cpp:279) bit for bit, including the t == 0
+//    case where the reference adds +0.
+struct QDesc {
+  int kn_off, n, val_off, ncombo;
+  int table;          // store table index (-1: missing)
+  int is_cell, op;
+  uint32_t clamp_tw;  // cells: tasks/width clamp bits (2..5), reported per query
   double wj[kMaxCombos], wk[kMaxCombos];
-  double tasks, width, scale;
-  uint32_t clamp_tw;    // tasks/width clamp bits (2..5), reported on every query
+  double scale;       // cells: token_scale; curves: payload_bytes_per_token
+  double share;       // curves: token_share (p2p: 1.0, exact)
+  double emul;        // energy multiplier: stage_devices / groups_per_stage / 1 (p2p)
+  double tasks, width;
 };
 
 // Trilinear sample with the reference's skip-zero-weight loop order:
 // acc += ((wi*wj)*wk)*v over ci, then the (cj, ck) corners.
-__device__ __forceinline__ void sample_cell(const CellConst& c, const AxisPos& pi,
-                                            double& sec, double& joule) {
+// The reference skips zero-weight corners; adding them instead is bit-
+// identical because every table value is finite and >= 0 (loaders reject
+// negatives), so a skipped term is an exact +0 and acc + (+0) == acc for the
+// non-negative accumulator.  Dropping the skip removes two data-dependent
+// branches (~20 cycles each on B200) from every query.
+__device__ __forceinline__ void sample(const QDesc& d, const double* vals, const AxisPos& pi,
+                                       double& sec, double& joule) {
   double as = 0.0, aj = 0.0;
 #pragma unroll
   for (int ci = 0; ci < 2; ++ci) {
     const double wi = ci ? pi.t : __dsub_rn(1.0, pi.t);
-    if (wi == 0.0) continue;
-    const double* v = c.vals + (ci ? pi.hi : pi.lo) * c.ncombo * 2;
-    for (int k = 0; k < c.ncombo; ++k) {
-      const double w = __dmul_rn(__dmul_rn(wi, c.wj[k]), c.wk[k]);
-      as = __dadd_rn(as, __dmul_rn(w, v[2 * k]));
-      aj = __dadd_rn(aj, __dmul_rn(w, v[2 * k + 1]));
+    const double* v = vals + (ci ? pi.hi : pi.lo) * d.ncombo * 2;
+#pragma unroll
+    for (int k = 0; k < kMaxCombos; ++k) {
+      if (k < d.ncombo) {
+        const double w = __dmul_rn(__dmul_rn(wi, d.wj[k]), d.wk[k]);
+        as = __dadd_rn(as, __dmul_rn(w, v[2 * k]));
+        aj = __dadd_rn(aj, __dmul_rn(w, v[2 * k + 1]));
+      }
     }
   }
   sec = as;
@@ -205,25 +240,6 @@ __device__ __forceinline__ double op_bytes(int op, double t, double k, double w,
   if (op == PSG_OP_ATTENTION)
     b = __dadd_rn(b, __dmul_rn(__dmul_rn(__dmul_rn(t, k), kv_elems), e));
   return b;
-}
-
-// A staged collective curve (payload knots, seconds, joules) with the
-// resolved collective's payload factors: payload = (ppt * tokens) * share,
-// energy multiplier = groups_per_stage (1 for p2p).
-struct CurveConst {
-  const double *x, *s, *j;
-  double ppt, share, emul;
-  int n, table;
-};
-
-// (1-t)*s[lo] + t*s[hi] (cost.cpp:279, :290).
-__device__ __forceinline__ void sample_curve(const CurveConst& c, double x, double& sec,
-                                             double& joule, int& clamp) {
-  const AxisPos p = locate(c.x, c.n, x);
-  clamp = p.clamp;
-  const double u = __dsub_rn(1.0, p.t);
-  sec = __dadd_rn(__dmul_rn(u, c.s[p.lo]), __dmul_rn(p.t, c.s[p.hi]));
-  joule = __dadd_rn(__dmul_rn(u, c.j[p.lo]), __dmul_rn(p.t, c.j[p.hi]));
 }
 
 }  // namespace psg

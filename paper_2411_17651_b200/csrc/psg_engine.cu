@@ -484,8 +484,9 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     tab_cap = std::max(tab_cap, sim_tab_doubles(int(nctx.size()), nctx.data(), int(ncurve.size()),
                                                 ncurve.data()));
   }
-  const int tab_smem = tab_cap * sizeof(double) <= 64 * 1024 ? int(tab_cap) : 0;
-  if (!tab_smem) PSG_CUDA(ctx->d_tab.ensure(tab_cap * sizeof(double) * std::max(n_units, 1)));
+  if (tab_cap * sizeof(double) > 96 * 1024)
+    return fail(ctx, PSG_ERR_USAGE, "profile tables of one plan exceed on-chip staging (96 KB)");
+  const int tab_smem = int(tab_cap);
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
   Packer wk;  // offsets only
   const size_t w_uout = wk.add<UnitOut>(nullptr, n_units), w_eout = wk.add<EntryOut>(nullptr, E),

@@ -6,24 +6,26 @@
 //
 // B200 design:
 //  * Scalar state is warp-uniform (every lane holds the same clock/energy),
-//    so there is no broadcast; batch scans (finish compaction, prefill
-//    advance, min-finish) are lane-parallel over the active list with
-//    ballot/popc compaction that keeps admission order and REDUX reductions.
-//  * Everything a unit touches per event lives in shared memory: the active
-//    list (SoA; migrates to a global region only if the batch outgrows it),
-//    a 32-request prefetch window of the replica's upcoming arrivals, and its
-//    cost tables — each cell's compute grid collapsed to the context axis at
-//    the cell's fixed (tasks, width) corners, each collective / distinct p2p
-//    curve — staged once at unit start.
+//    so there is no broadcast; batch scans are lane-parallel over the active
+//    slots with ballot/popc and REDUX reductions.
+//  * Shared memory holds everything an event touches: the active slots
+//    (SoA, tombstoned, migrating to a global region only if the batch
+//    outgrows them), a 32-request prefetch window of the replica's arrivals,
+//    the decode-cost memo, and the unit's cost tables — every cell's compute
+//    grid collapsed to its fixed (tasks, width) corners, every collective and
+//    distinct p2p curve — staged once at unit start.
+//  * The KV ledger is an exact integer: cap_tok = max{T : double(T)*kv <= cap}
+//    turns every admission / overflow / admissibility test into an integer
+//    compare and every event horizon into one integer division.
 //  * Exact event-driven macro-stepping: a decode-only iteration's workload is
 //    {decode_count = B}, so its (seconds, joules, flops, bytes) are bit-
 //    identical until the batch changes.  Between events (arrival of an
 //    admissible/rejectable head, first finish, first KV overflow) the unit
 //    runs a tight loop of the reference's sequential FP64 adds only.
-//  * Costs: per-query locate/interpolate is lane-parallel; accumulation is
-//    serial in the reference's order (cells -> items in admission order ->
-//    decode, then collectives, then per-stage p2p), never a tree reduction.
-//    A shared-memory memo caches decode-only costs per batch size.
+//  * Cost queries of one iteration run one per lane through a single
+//    divergence-free path (cells and curves share locate + sample); their
+//    accumulation is serial in the reference's order (cells -> items in
+//    admission order -> decode, collectives, then per-stage p2p).
 #include <climits>
 
 #include "psg_device.cuh"
@@ -32,33 +34,14 @@ namespace psg {
 
 namespace {
 
-constexpr int64_t kNoFin = INT64_MAX;   // prefill phase
-constexpr int64_t kDead = INT64_MIN;    // tombstone (finished / evicted slot)
+constexpr int64_t kNoFin = INT64_MAX;  // prefill phase
+constexpr int64_t kDead = INT64_MIN;   // tombstone (finished / evicted slot)
 constexpr unsigned kNoRel = 0xffffffffu;
 constexpr int kGI32 = 7;  // global fallback arrays: stack, tidx, ctx, gen, done, slot, items
 constexpr int kGF64 = 4;  // adm, ft, arr, fin
 
-__device__ __forceinline__ double dmax_ref(double a, double b) {
-  return (a < b) ? b : a;  // std::max(a, b)
-}
-
-struct PlanConst {
-  double kv, cap, reps, sdd, Sd, p2p_ppt, hidden, head_dim, kv_elems;
-  int S, C, K, NB, ND, c0, k0, b0;
-};
-
-struct ActiveList {
-  int32_t *tidx, *ctx, *gen, *done, *slot, *items;
-  int64_t* fin;  // iteration index of the finishing decode step; kNoFin while prefilling
-  double *adm, *ft, *arr;
-};
-
-struct Cost {
-  double dur, energy, flops, bytes;
-};
-
 // Phase profiler (dev builds only: -DPSG_PHASE_PROFILE; zero code otherwise).
-// slots: 0 admit, 1 mixed scan, 2 mixed eval, 3 mixed advance, 4 decode cost,
+// slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 unused,
 // 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
 // 11 #decode runs, 12 #decode evals, 13 #finish events, 14 unused, 15 total.
 #ifdef PSG_PHASE_PROFILE
@@ -71,20 +54,28 @@ struct Cost {
 #define PROF_CNT(slot)
 #endif
 
+__device__ __forceinline__ double dmax_ref(double a, double b) {
+  return (a < b) ? b : a;  // std::max(a, b)
+}
+
+struct ActiveList {
+  int32_t *tidx, *ctx, *gen, *done, *slot, *items;
+  int64_t* fin;  // iteration index of the finishing decode step; kNoFin while prefilling
+  double *adm, *ft, *arr;
+};
+
 __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct SmemLayout {
-  size_t qv, pc, cc, cv, p2p_slot, p2p_val, combo, clamp, win_arr, win_i32, memo, act_f64,
-      act_fin, act_i32, tab, total;
+  size_t qv, desc, p2p_slot, p2p_val, combo, clamp, win_arr, win_i32, memo, act_f64, act_fin,
+      act_i32, tab, total;
 };
 
 __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem) {
   SmemLayout L;
   size_t o = 0;
   L.qv = o;        o = al16(o + sizeof(double) * 4 * kWarp);
-  L.pc = o;        o = al16(o + sizeof(PlanConst));
-  L.cc = o;        o = al16(o + sizeof(CellConst) * kMaxCells);
-  L.cv = o;        o = al16(o + sizeof(CurveConst) * kMaxClampSlots);
+  L.desc = o;      o = al16(o + sizeof(QDesc) * kMaxClampSlots);
   L.p2p_slot = o;  o = al16(o + kMaxClampSlots);
   L.p2p_val = o;   o = al16(o + sizeof(double) * 2 * kMaxClampSlots);
   L.combo = o;     o = al16(o + sizeof(int32_t) * kMaxCells * kMaxCombos);
@@ -100,97 +91,17 @@ __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_s
   return L;
 }
 
-// Lane-parallel query evaluation + reference-ordered serial accumulation of
-// one iteration (iteration_time, simulator.cpp:17-87).  Kept out of line: the
-// kernel calls it from the mixed and the decode path, and the instruction
-// cache is the scarcer resource for one-warp-per-SMSP latency-bound code.
-__device__ __noinline__ Cost eval_iteration(const PlanConst* __restrict__ pc,
-                                            const CellConst* __restrict__ cc,
-                                            const CurveConst* __restrict__ cv,
-                                            const uint8_t* __restrict__ p2p_slot,
-                                            double* p2p_val, const int32_t* items,
-                                            int n_items, int64_t decode, int64_t total,
-                                            double* qv, uint32_t* clampbits) {
-  const int lane = threadIdx.x;
-  const int C = pc->C, K = pc->K, ND = pc->ND;
-  const int nq_c = n_items + (decode > 0 ? 1 : 0);
-  const int Qc = C * nq_c;
-  const int Q = Qc + K + ND;
-  const double total_d = double(total);
-  const double sdd = pc->sdd;
-
-  double bs = 0.0, bj = 0.0, bf = 0.0, bb = 0.0;
-  for (int base = 0; base < Q; base += kWarp) {
-    const int q = base + lane;
-    if (q < Q) {
-      double t, en, fl = 0.0, by = 0.0;
-      if (q < Qc) {
-        const int c = q / nq_c;
-        const int i = q - c * nq_c;
-        const int64_t tok = i < n_items ? int64_t(items[i]) : decode;
-        const CellConst& cell = cc[c];
-        const double x = __dmul_rn(double(tok), cell.scale);
-        const AxisPos pi = locate(cell.knots, cell.n_ctx, x);
-        sample_cell(cell, pi, t, en);
-        en = __dmul_rn(en, sdd);  // query_energy * stage_devices
-        fl = op_flops(cell.op, x, cell.tasks, cell.width, pc->hidden, pc->head_dim);
-        by = op_bytes(cell.op, x, cell.tasks, cell.width, pc->hidden, pc->kv_elems);
-        const uint32_t bits =
-            (pi.clamp < 0 ? 1u : 0u) | (pi.clamp > 0 ? 2u : 0u) | cell.clamp_tw;
-        if (bits) atomicOr(&clampbits[c], bits);
-      } else {
-        const int k = q - Qc;  // K collectives, then ND distinct p2p curves
-        const CurveConst& cu = cv[k];
-        const double payload = __dmul_rn(__dmul_rn(cu.ppt, total_d), cu.share);
-        int clamp;
-        sample_curve(cu, payload, t, en, clamp);
-        if (k < K) {
-          en = __dmul_rn(en, cu.emul);  // query_energy * groups_per_stage
-        } else {
-          p2p_val[k - K] = t;
-          p2p_val[kMaxClampSlots + k - K] = en;
-        }
-        if (clamp) atomicOr(&clampbits[C + k], clamp < 0 ? 1u : 2u);
-      }
-      qv[lane] = t;
-      qv[kWarp + lane] = en;
-      qv[2 * kWarp + lane] = fl;
-      qv[3 * kWarp + lane] = by;
-    }
-    __syncwarp();
-    const int here = min(kWarp, Q - base);
-    const int cell_end = min(here, max(0, Qc - base));
-    const int coll_end = min(here, max(0, Qc + K - base));
-    int l = 0;
-    for (; l < cell_end; ++l) {
-      bs = __dadd_rn(bs, qv[l]);
-      bj = __dadd_rn(bj, qv[kWarp + l]);
-      bf = __dadd_rn(bf, qv[2 * kWarp + l]);
-      bb = __dadd_rn(bb, qv[3 * kWarp + l]);
-    }
-    for (; l < coll_end; ++l) {
-      bs = __dadd_rn(bs, qv[l]);
-      bj = __dadd_rn(bj, qv[kWarp + l]);
-    }
-    __syncwarp();
-  }
-  // ---- stages (simulator.cpp:64-78, :125-130): every stage prices the same
-  // block * reps; boundary b adds its p2p to stage b+1 ----
-  const double srep = __dmul_rn(bs, pc->reps);
-  const double jrep = __dmul_rn(bj, pc->reps);
-  double d = dmax_ref(0.0, srep);
-  double e = __dadd_rn(0.0, jrep);
-  for (int b = 0; b < pc->NB; ++b) {
-    const int s = p2p_slot[b];
-    d = dmax_ref(d, __dadd_rn(srep, p2p_val[s]));
-    e = __dadd_rn(e, __dadd_rn(jrep, p2p_val[kMaxClampSlots + s]));
-  }
-  Cost r;
-  r.dur = d;
-  r.energy = e;
-  r.flops = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), pc->reps), pc->Sd);
-  r.bytes = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), pc->reps), pc->Sd);
-  return r;
+// max{T >= -1 : double(T) * kv <= cap} with the reference's exact product
+// (kv is integral and every ledger value < 2^53, checked on the host).
+__device__ int64_t ledger_cap_tokens(double kv, double cap) {
+  if (!(kv > 0.0)) return (0.0 <= cap) ? (int64_t(1) << 60) : -1;
+  if (!(0.0 <= cap)) return -1;
+  const double q = floor(cap / kv);
+  if (q >= 9007199254740992.0) return int64_t(1) << 53;  // beyond any ledger value
+  int64_t t = int64_t(q);
+  while (t >= 0 && __dmul_rn(double(t), kv) > cap) --t;
+  while (!(__dmul_rn(double(t + 1), kv) > cap)) ++t;
+  return t;
 }
 
 }  // namespace
@@ -207,9 +118,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem);
   double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
-  PlanConst* pcs = reinterpret_cast<PlanConst*>(smem_raw + L.pc);
-  CellConst* cc = reinterpret_cast<CellConst*>(smem_raw + L.cc);
-  CurveConst* cv = reinterpret_cast<CurveConst*>(smem_raw + L.cv);
+  QDesc* desc = reinterpret_cast<QDesc*>(smem_raw + L.desc);
   uint8_t* p2p_slot = reinterpret_cast<uint8_t*>(smem_raw + L.p2p_slot);
   double* p2p_val = reinterpret_cast<double*>(smem_raw + L.p2p_val);
   int32_t* combo = reinterpret_cast<int32_t*>(smem_raw + L.combo);
@@ -217,149 +126,147 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   double* w_arr = reinterpret_cast<double*>(smem_raw + L.win_arr);
   int32_t* w_i32 = reinterpret_cast<int32_t*>(smem_raw + L.win_i32);  // tidx, ctx, gen, slot
   double* memo = reinterpret_cast<double*>(smem_raw + L.memo);
-  double* tab = p.tab_smem > 0 ? reinterpret_cast<double*>(smem_raw + L.tab)
-                               : p.g_tab + size_t(blockIdx.x) * size_t(p.tab_cap);
+  double* tab = reinterpret_cast<double*>(smem_raw + L.tab);
 
-  // ---- plan constants (warp-uniform, also staged for the evaluator) ----
+  // ---- plan constants (warp-uniform) ----
   const int pl = U.plan;
-  PlanConst pc;
-  pc.kv = p.P.kv[pl];
-  pc.cap = p.P.budget[pl];
-  pc.S = p.P.num_stages[pl];
-  pc.reps = double(p.P.stage_reps[pl]);
-  pc.sdd = double(p.P.stage_devices[pl]);
-  pc.Sd = double(pc.S);
-  pc.p2p_ppt = p.P.p2p_ppt[pl];
-  pc.hidden = p.P.sh_hidden[pl];
-  pc.head_dim = p.P.sh_head[pl];
-  pc.kv_elems = p.P.sh_kv[pl];
-  pc.c0 = p.P.cell_begin[pl];
-  pc.C = p.P.cell_begin[pl + 1] - pc.c0;
-  pc.k0 = p.P.coll_begin[pl];
-  pc.K = p.P.coll_begin[pl + 1] - pc.k0;
-  pc.b0 = p.P.p2p_begin[pl];
-  pc.NB = p.P.p2p_begin[pl + 1] - pc.b0;
-  // distinct p2p tables (boundaries only span 1 or 2 nodes in practice)
+  const double kv = p.P.kv[pl], cap = p.P.budget[pl];
+  const int S = p.P.num_stages[pl];
+  const double reps = double(p.P.stage_reps[pl]);
+  const double sdd = double(p.P.stage_devices[pl]);
+  const double Sd = double(S);
+  const double p2p_ppt = p.P.p2p_ppt[pl];
+  const double hidden = p.P.sh_hidden[pl], head_dim = p.P.sh_head[pl], kv_elems = p.P.sh_kv[pl];
+  const int c0 = p.P.cell_begin[pl], C = p.P.cell_begin[pl + 1] - c0;
+  const int k0 = p.P.coll_begin[pl], K = p.P.coll_begin[pl + 1] - k0;
+  const int b0 = p.P.p2p_begin[pl], NB = p.P.p2p_begin[pl + 1] - b0;
+  const int64_t cap_tok = ledger_cap_tokens(kv, cap);
+
+  // distinct p2p tables: boundaries only span 1 or 2 nodes in practice
   int ND = 0;
-  {
-    int dist_tab[kMaxClampSlots];
-    for (int b = 0; b < pc.NB; ++b) {
-      const int t = p.p2p_tab[pc.b0 + b];
-      int s = 0;
-      while (s < ND && dist_tab[s] != t) ++s;
-      if (s == ND) dist_tab[ND++] = t;
-      if (lane == 0) p2p_slot[b] = uint8_t(s);
+  for (int b = 0; b < NB; ++b) {
+    const int t = p.p2p_tab[b0 + b];
+    int s = 0;
+    for (; s < ND; ++s)
+      if (desc[C + K + s].table == t) break;
+    if (s == ND) {
+      if (lane == 0) desc[C + K + ND].table = t;
+      ++ND;
+      __syncwarp();
     }
-    pc.ND = ND;
-    for (int s = lane; s < ND; s += kWarp) {
-      CurveConst c;
-      c.table = dist_tab[s];
-      cv[pc.K + s] = c;
-    }
+    if (lane == 0) p2p_slot[b] = uint8_t(s);
   }
-  if (lane == 0) *pcs = pc;
-  for (int s = lane; s < kMaxClampSlots; s += kWarp) clampbits[s] = 0;
+  const int NQ = C + K + ND;  // descriptors: cells, collectives, distinct p2p
+  uint64_t p2p_mask = 0;      // ND <= 2: bit b = distinct-table slot of boundary b
+  __syncwarp();
+  for (int b = 0; b < NB && ND <= 2; ++b) p2p_mask |= uint64_t(p2p_slot[b]) << b;
+  for (int s = lane; s < kMaxClampSlots; s += kWarp) {
+    clampbits[s] = 0;
+  }
   for (int i = lane; i < 4 * p.memo_cap; i += kWarp) memo[i] = -1.0;
+  __syncwarp();
 
-  // ---- stage the unit's tables ----
-  if (lane < pc.C) {
-    CellConst c;
-    const int g = pc.c0 + lane;
-    c.table = p.cell_tab[size_t(U.fslot) * p.n_cells_total + g];
-    c.op = p.P.cell_op[g];
-    c.tasks = p.P.cell_tasks[g];
-    c.width = p.P.cell_width[g];
-    c.scale = p.P.cell_scale[g];
-    c.ncombo = 0;
-    c.clamp_tw = 0;
-    c.n_ctx = 1;
-    if (c.table >= 0) {
-      c.n_ctx = p.S.c_n_ctx[c.table];
-      const int nt = p.S.c_n_tasks[c.table], nw = p.S.c_n_width[c.table];
-      const double* kn = p.S.c_knots + p.S.c_knot_begin[c.table];
-      const AxisPos pj = locate(kn + c.n_ctx, nt, c.tasks);
-      const AxisPos pk = locate(kn + c.n_ctx + nt, nw, c.width);
-      c.clamp_tw = uint32_t(pj.clamp < 0) << 2 | uint32_t(pj.clamp > 0) << 3 |
-                   uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
-      for (int cj = 0; cj < 2; ++cj) {
-        const double wj = cj ? pj.t : __dsub_rn(1.0, pj.t);
-        if (wj == 0.0) continue;
-        for (int ck = 0; ck < 2; ++ck) {
-          const double wk = ck ? pk.t : __dsub_rn(1.0, pk.t);
-          if (wk == 0.0) continue;
-          c.wj[c.ncombo] = wj;
-          c.wk[c.ncombo] = wk;
-          combo[lane * kMaxCombos + c.ncombo] = (cj ? pj.hi : pj.lo) * nw + (ck ? pk.hi : pk.lo);
-          ++c.ncombo;
+  // ---- stage the unit's tables (QDesc + values in shared memory) ----
+  if (lane < NQ) {
+    QDesc d;
+    d.ncombo = 1;
+    d.wj[0] = d.wk[0] = 1.0;
+    d.clamp_tw = 0;
+    d.tasks = d.width = 0.0;
+    d.op = 0;
+    if (lane < C) {
+      const int g = c0 + lane;
+      d.is_cell = 1;
+      d.table = p.cell_tab[size_t(U.fslot) * p.n_cells_total + g];
+      d.op = p.P.cell_op[g];
+      d.tasks = p.P.cell_tasks[g];
+      d.width = p.P.cell_width[g];
+      d.scale = p.P.cell_scale[g];
+      d.share = 1.0;
+      d.emul = sdd;  // query_energy * stage_devices
+      d.n = 1;
+      d.ncombo = 0;
+      if (d.table >= 0) {
+        d.n = p.S.c_n_ctx[d.table];
+        const int nt = p.S.c_n_tasks[d.table], nw = p.S.c_n_width[d.table];
+        const double* kn = p.S.c_knots + p.S.c_knot_begin[d.table];
+        const AxisPos pj = locate(kn + d.n, nt, d.tasks);
+        const AxisPos pk = locate(kn + d.n + nt, nw, d.width);
+        d.clamp_tw = uint32_t(pj.clamp < 0) << 2 | uint32_t(pj.clamp > 0) << 3 |
+                     uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
+        for (int cj = 0; cj < 2; ++cj) {
+          const double wj = cj ? pj.t : __dsub_rn(1.0, pj.t);
+          if (wj == 0.0) continue;
+          for (int ck = 0; ck < 2; ++ck) {
+            const double wk = ck ? pk.t : __dsub_rn(1.0, pk.t);
+            if (wk == 0.0) continue;
+            d.wj[d.ncombo] = wj;
+            d.wk[d.ncombo] = wk;
+            combo[lane * kMaxCombos + d.ncombo] = (cj ? pj.hi : pj.lo) * nw + (ck ? pk.hi : pk.lo);
+            ++d.ncombo;
+          }
         }
       }
+    } else {
+      d.is_cell = 0;
+      if (lane < C + K) {
+        const int g = k0 + lane - C;
+        d.table = p.coll_tab[g];
+        d.scale = p.P.coll_ppt[g];
+        d.share = p.P.coll_share[g];
+        d.emul = double(p.P.coll_groups[g]);  // query_energy * groups_per_stage
+      } else {
+        d.table = desc[lane].table;
+        d.scale = p2p_ppt;  // payload = p2p_ppt * tokens; x * 1.0 is exact
+        d.share = 1.0;
+        d.emul = 1.0;
+      }
+      d.n = d.table >= 0 ? p.S.k_n[d.table] : 1;
     }
-    cc[lane] = c;
-  }
-  for (int k = lane; k < pc.K; k += kWarp) {
-    const int g = pc.k0 + k;
-    CurveConst c;
-    c.table = p.coll_tab[g];
-    c.ppt = p.P.coll_ppt[g];
-    c.share = p.P.coll_share[g];
-    c.emul = double(p.P.coll_groups[g]);
-    cv[k] = c;
-  }
-  for (int s = lane; s < ND; s += kWarp) {
-    cv[pc.K + s].ppt = pc.p2p_ppt;
-    cv[pc.K + s].share = 1.0;  // payload = p2p_ppt * tokens; x * 1.0 is exact
-    cv[pc.K + s].emul = 1.0;
+    desc[lane] = d;
   }
   __syncwarp();
   {
-    size_t off = 0;
-    for (int c = 0; c < pc.C; ++c) {
-      const CellConst cl = cc[c];
+    int off = 0;
+    for (int q = 0; q < NQ; ++q) {
+      const int n = desc[q].n, nc = desc[q].ncombo, t = desc[q].table;
       double* kd = tab + off;
-      double* vd = kd + cl.n_ctx;
-      if (cl.table >= 0) {
-        const double* kn = p.S.c_knots + p.S.c_knot_begin[cl.table];
-        const double* vs = p.S.c_seconds + p.S.c_value_begin[cl.table];
-        const double* vj = p.S.c_joules + p.S.c_value_begin[cl.table];
-        const int plane = p.S.c_n_tasks[cl.table] * p.S.c_n_width[cl.table];
-        for (int i = lane; i < cl.n_ctx; i += kWarp) kd[i] = kn[i];
-        for (int i = lane; i < cl.n_ctx * cl.ncombo; i += kWarp) {
-          const int r = i / cl.ncombo, cb = i - r * cl.ncombo;
-          const int64_t v = int64_t(r) * plane + combo[c * kMaxCombos + cb];
-          vd[2 * i] = vs[v];
-          vd[2 * i + 1] = vj[v];
-        }
-      }
-      if (lane == 0) {
-        cc[c].knots = kd;
-        cc[c].vals = vd;
-      }
-      off += size_t(cl.n_ctx) * (1 + 2 * cl.ncombo);
-    }
-    for (int k = 0; k < pc.K + ND; ++k) {
-      const int t = cv[k].table;
-      const int n = t >= 0 ? p.S.k_n[t] : 1;
-      double* x = tab + off;
+      double* vd = kd + n;
       if (t >= 0) {
-        const int64_t b = p.S.k_begin[t];
-        for (int i = lane; i < n; i += kWarp) {
-          x[i] = p.S.k_payload[b + i];
-          x[n + i] = p.S.k_seconds[b + i];
-          x[2 * n + i] = p.S.k_joules[b + i];
+        if (q < C) {
+          const double* kn = p.S.c_knots + p.S.c_knot_begin[t];
+          const double* vs = p.S.c_seconds + p.S.c_value_begin[t];
+          const double* vj = p.S.c_joules + p.S.c_value_begin[t];
+          const int plane = p.S.c_n_tasks[t] * p.S.c_n_width[t];
+          for (int i = lane; i < n; i += kWarp) kd[i] = kn[i];
+          for (int i = lane; i < n * nc; i += kWarp) {
+            const int r = i / nc, cb = i - r * nc;
+            const int64_t v = int64_t(r) * plane + combo[q * kMaxCombos + cb];
+            vd[2 * i] = vs[v];
+            vd[2 * i + 1] = vj[v];
+          }
+        } else {
+          const int64_t b = p.S.k_begin[t];
+          for (int i = lane; i < n; i += kWarp) {
+            kd[i] = p.S.k_payload[b + i];
+            vd[2 * i] = p.S.k_seconds[b + i];
+            vd[2 * i + 1] = p.S.k_joules[b + i];
+          }
         }
       }
       if (lane == 0) {
-        cv[k].x = x;
-        cv[k].s = x + n;
-        cv[k].j = x + 2 * n;
-        cv[k].n = n;
+        desc[q].kn_off = off;
+        desc[q].val_off = off + n;
       }
-      off += 3 * size_t(n);
+      off += n * (1 + 2 * nc);
     }
   }
   __syncwarp();
 
-  // ---- active list ----
+  int n_knots_max = 1;  // longest knot axis among the unit's tables
+  for (int q = 0; q < NQ; ++q) n_knots_max = max(n_knots_max, desc[q].n);
+
+  // ---- active slots ----
   int cap_now = p.smem_cap;
   ActiveList a;
   {
@@ -387,8 +294,6 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
                    : int(int64_t(U.replica) + int64_t(j) * U.replicas);
   };
   const size_t slot_base = size_t(U.entry) * size_t(p.n_slots);
-
-  const double kv = pc.kv, cap = pc.cap;
   const bool chunked = p.batch_mode == PSG_BATCH_CHUNKED;
   const int64_t chunk = p.chunk_size;
   const int64_t max_bs = p.max_batch_size;
@@ -398,10 +303,10 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   double clock = 0.0, energy = 0.0, flops = 0.0, bytes = 0.0;
   int64_t n = 0, max_batch = 0, completed = 0, rejected = 0, sum_batch = 0, admissions = 0;
   int pend = 0, stack_top = 0, w_base = -kWindow;
-  // Active slots in admission order with tombstones: B live of len used,
+  // Active slots in admission order with tombstones: B live of len used;
   // live slots below first_pre are all decode-phase (prefill frontier).
   int B = 0, len = 0, first_pre = 0, n_pre = 0;
-  int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated)
+  int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated) <= cap_tok
   int64_t next_fin = kNoFin;
   int err = 0;
 
@@ -443,9 +348,6 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     hd_ctx = w_i32[kWindow + w];
     hd_gen = w_i32[2 * kWindow + w];
     hd_slot = w_i32[3 * kWindow + w];
-  };
-  auto fits = [&](int64_t tokens) -> bool {  // double(tokens) * kv <= cap, exact
-    return !(__dmul_rn(double(tokens), kv) > cap);
   };
   auto reject_slot = [&](int slot) {
     if (lane == 0) p.slot_status[slot_base + slot] = 2;
@@ -548,85 +450,15 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     }
     next_fin = m == kNoRel ? kNoFin : n + m;
   };
-  // Finish removal (batching.cpp:95-102) + metrics (simulator.cpp:143-156),
-  // then LIFO eviction (batching.cpp:110-125), at iteration n after the clock
-  // has advanced.  Finished slots become tombstones.
-  auto finish_and_evict = [&]() {
-    PROF_T0(t_fin);
-    if (next_fin == n) {
-      PROF_CNT(13);
-      int64_t freed = 0;
-      unsigned m = kNoRel, nfin = 0;
-      for (int base = 0; base < len; base += kWarp) {
-        const int i = base + lane;
-        const int64_t fin = i < len ? a.fin[i] : kDead;
-        const bool fnow = fin == n;
-        unsigned tok = 0;
-        if (fnow) {
-          const int32_t gen = a.gen[i];
-          const double arr = a.arr[i], ft = a.ft[i];
-          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
-          const size_t s = slot_base + a.slot[i];
-          p.slot_e2e[s] = __dsub_rn(clock, arr);
-          p.slot_ttft[s] = __dsub_rn(ft, anchor);
-          p.slot_tpot[s] = gen >= 2 ? __ddiv_rn(__dsub_rn(clock, ft), double(gen - 1)) : 0.0;
-          p.slot_status[s] = 1;
-          a.fin[i] = kDead;
-          tok = unsigned(a.ctx[i] + gen);
-        }
-        freed += int64_t(__reduce_add_sync(kFull, tok));
-        nfin += __popc(__ballot_sync(kFull, fnow));
-        m = min(m, __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n)));
-      }
-      B -= int(nfin);
-      completed += nfin;
-      used -= freed;
-      next_fin = m == kNoRel ? kNoFin : n + m;
-      trim();
-      if (len > 2 * B + 2 * kWarp) compact();
-    }
-    PROF_ADD(7, t_fin);
-    PROF_T0(t_ev);
-    bool evicted = false;
-    while (B > 1 && !fits(used)) {
-      const int i = len - 1;  // newest live request (trim invariant)
-      const int64_t fin = a.fin[i];
-      const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
-      used -= int64_t(a.ctx[i]) + tok;
-      if (fin == kNoFin) --n_pre;
-      if (lane == 0) {
-        g_stack[stack_top] = a.tidx[i];  // push_front of pending
-        a.fin[i] = kDead;
-      }
-      ++stack_top;
-      --B;
-      evicted = true;
-      trim();
-    }
-    if (B == 1 && !fits(used)) {
-      reject_slot(a.slot[len - 1]);
-      B = len = first_pre = n_pre = 0;
-      used = 0;
-      next_fin = kNoFin;
-      evicted = false;
-    }
-    __syncwarp();
-    if (evicted) {
-      load_head();
-      recompute_next_fin();
-    }
-    PROF_ADD(8, t_ev);
-  };
 
   load_head();
   while (true) {
     // ---- admit (batching.cpp:35-60) ----
     PROF_T0(t_adm);
     while (hd_valid && hd_arr <= clock) {
-      const bool reject = __dmul_rn(double(hd_ctx), kv) > cap;
-      if (!reject) {
+      if (hd_ctx <= cap_tok) {  // context alone fits; else rejected below
         if (max_bs > 0 && int64_t(B) >= max_bs) break;
-        if (!fits(used + hd_ctx)) break;
+        if (used + hd_ctx > cap_tok) break;  // head blocks, FIFO
         if (len >= cap_now) {
           if (len > B) compact();
           if (len >= cap_now) migrate();
@@ -664,14 +496,15 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     if (chunk_err) { err = 1; break; }
     if (missing) { err = 2; break; }
 
-    bool settle = true;
-    if (n_pre > 0) {
-      // ---- mixed iteration: literal step (batching.cpp:62-108) over the
-      // prefill frontier only ----
+    // ---- the iteration's workload (batching.cpp:67-76) ----
+    const bool mixed = n_pre > 0;
+    int n_items = 0;
+    int64_t pre_tok = 0;
+    double cd = 0.0, ce = 0.0, cf = 0.0, cb = 0.0;  // duration, energy, flops, bytes
+    bool need_eval = true;
+    if (mixed) {
       PROF_CNT(10);
       PROF_T0(t_m1);
-      int n_items = 0;
-      int64_t pre_tok = 0;
       for (int base = first_pre; base < len; base += kWarp) {
         const int i = base + lane;
         const bool pre = i < len && a.fin[i] == kNoFin;
@@ -687,17 +520,161 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
         pre_tok += __reduce_add_sync(kFull, unsigned(tok));
       }
       __syncwarp();
-      const int64_t decode = int64_t(B) - n_items;
       PROF_ADD(1, t_m1);
-      PROF_T0(t_m2);
-      const Cost c = eval_iteration(pcs, cc, cv, p2p_slot, p2p_val, a.items, n_items, decode,
-                                    decode + pre_tok, qv, clampbits);
-      PROF_ADD(2, t_m2);
+    } else {
+      PROF_CNT(11);
+      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
+        cd = memo[4 * (B - 1)];
+        ce = memo[4 * (B - 1) + 1];
+        cf = memo[4 * (B - 1) + 2];
+        cb = memo[4 * (B - 1) + 3];
+        need_eval = false;
+      } else {
+        PROF_CNT(12);
+      }
+    }
+    const int64_t decode = int64_t(B) - n_items;
+
+    if (need_eval) {
+      // ---- iteration_time (simulator.cpp:17-87) ----
+      PROF_T0(t_ev);
+      const int nq_c = n_items + (decode > 0 ? 1 : 0);
+      const int Qc = C * nq_c;
+      const int Q = Qc + K + ND;
+      const double total_d = double(decode + pre_tok);
+      double bs = 0.0, bj = 0.0, bf = 0.0, bb = 0.0;
+      for (int base = 0; base < Q; base += kWarp) {
+        const int q = base + lane;
+        {
+          // Convergent straight-line query: every lane runs the same code
+          // (selects instead of branches); lanes past Q compute a dummy.
+          const bool act = q < Q;
+          const bool cellq = q < Qc;
+          const int cdi = cellq ? q / nq_c : 0;
+          const int item = q - cdi * nq_c;
+          const int di = act ? (cellq ? cdi : C + (q - Qc)) : 0;
+          const int64_t tok =
+              (cellq && item < n_items) ? int64_t(a.items[cellq ? item : 0]) : decode;
+          const QDesc& d = desc[di];
+          // cell: tokens * token_scale; curve: (ppt * tokens) * share
+          const double xc = __dmul_rn(double(tok), d.scale);
+          const double xk = __dmul_rn(__dmul_rn(d.scale, total_d), d.share);
+          const double x = d.is_cell ? xc : xk;
+          // locate (cost.cpp:85-102) by counting knots <= x: no data-
+          // dependent branches, independent loads
+          const double* kn = tab + d.kn_off;
+          const int n = d.n;
+          int cnt = 0;
+          for (int j = 0; j < n_knots_max; ++j) {
+            const double kj = kn[j < n ? j : n - 1];
+            cnt += (j < n && kj <= x) ? 1 : 0;
+          }
+          const double first = kn[0], last = kn[n - 1];
+          const bool lo_clamp = x <= first, hi_clamp = x >= last;
+          const int lo = lo_clamp ? 0 : (hi_clamp ? n - 1 : cnt - 1);
+          const int hi = lo_clamp ? 0 : (hi_clamp ? n - 1 : cnt);
+          const double klo = kn[lo], khi = kn[hi];
+          const bool interior = !(lo_clamp || hi_clamp);
+          AxisPos pi;
+          pi.lo = lo;
+          pi.hi = hi;
+          pi.t = __ddiv_rn(interior ? __dsub_rn(x, klo) : 0.0,
+                           interior ? __dsub_rn(khi, klo) : 1.0);
+          pi.clamp = x < first ? -1 : (x > last ? 1 : 0);
+          double t, en;
+          sample(d, tab + d.val_off, pi, t, en);
+          en = __dmul_rn(en, d.emul);
+          const double fl0 = op_flops(d.op, x, d.tasks, d.width, hidden, head_dim);
+          const double by0 = op_bytes(d.op, x, d.tasks, d.width, hidden, kv_elems);
+          const double fl = d.is_cell ? fl0 : 0.0, by = d.is_cell ? by0 : 0.0;
+          const uint32_t bits = (pi.clamp < 0 ? 1u : 0u) | (pi.clamp > 0 ? 2u : 0u) | d.clamp_tw;
+          if (act && bits) atomicOr(&clampbits[di], bits);
+          if (act && di >= C + K) {
+            p2p_val[di - C - K] = t;
+            p2p_val[kMaxClampSlots + di - C - K] = en;
+          }
+          qv[lane] = t;
+          qv[kWarp + lane] = en;
+          qv[2 * kWarp + lane] = fl;
+          qv[3 * kWarp + lane] = by;
+        }
+        __syncwarp();
+        const int here = min(kWarp, Q - base);
+        const int cell_end = min(here, max(0, Qc - base));
+        const int coll_end = min(here, max(0, Qc + K - base));
+        // loads first (independent), then the reference-ordered FP64 chains
+        int l = 0;
+        for (; l + 4 <= cell_end; l += 4) {
+          double t[4], e[4], f[4], y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            t[u] = qv[l + u];
+            e[u] = qv[kWarp + l + u];
+            f[u] = qv[2 * kWarp + l + u];
+            y[u] = qv[3 * kWarp + l + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            bs = __dadd_rn(bs, t[u]);
+            bj = __dadd_rn(bj, e[u]);
+            bf = __dadd_rn(bf, f[u]);
+            bb = __dadd_rn(bb, y[u]);
+          }
+        }
+        for (; l < cell_end; ++l) {
+          bs = __dadd_rn(bs, qv[l]);
+          bj = __dadd_rn(bj, qv[kWarp + l]);
+          bf = __dadd_rn(bf, qv[2 * kWarp + l]);
+          bb = __dadd_rn(bb, qv[3 * kWarp + l]);
+        }
+        for (; l < coll_end; ++l) {
+          bs = __dadd_rn(bs, qv[l]);
+          bj = __dadd_rn(bj, qv[kWarp + l]);
+        }
+        __syncwarp();
+      }
+      // stages (simulator.cpp:64-78, :125-130): every stage prices the same
+      // block * reps; boundary b adds its p2p to stage b+1
+      const double srep = __dmul_rn(bs, reps);
+      const double jrep = __dmul_rn(bj, reps);
+      cd = dmax_ref(0.0, srep);
+      ce = __dadd_rn(0.0, jrep);
+      if (ND <= 2) {
+        // stage b+1 = (block*reps) + p2p of its boundary's (at most two)
+        // distinct tables; max is exact in any order, energies add in order
+        const double s0 = __dadd_rn(srep, p2p_val[0]), s1 = __dadd_rn(srep, p2p_val[1]);
+        const double j0 = __dadd_rn(jrep, p2p_val[kMaxClampSlots]);
+        const double j1 = __dadd_rn(jrep, p2p_val[kMaxClampSlots + 1]);
+        if (NB > 0) cd = dmax_ref(cd, s0);
+        if (ND == 2) cd = dmax_ref(cd, s1);
+        for (int b = 0; b < NB; ++b) ce = __dadd_rn(ce, ((p2p_mask >> b) & 1) ? j1 : j0);
+      } else {
+        for (int b = 0; b < NB; ++b) {
+          const int s = p2p_slot[b];
+          cd = dmax_ref(cd, __dadd_rn(srep, p2p_val[s]));
+          ce = __dadd_rn(ce, __dadd_rn(jrep, p2p_val[kMaxClampSlots + s]));
+        }
+      }
+      cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
+      cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
+      if (!mixed && B <= p.memo_cap && lane == 0) {
+        memo[4 * (B - 1) + 1] = ce;
+        memo[4 * (B - 1) + 2] = cf;
+        memo[4 * (B - 1) + 3] = cb;
+        memo[4 * (B - 1)] = cd;
+      }
+      __syncwarp();
+      PROF_ADD(2, t_ev);
+    }
+
+    bool settle = true;
+    if (mixed) {
+      // ---- advance (batching.cpp:78-93) over the prefill frontier ----
       PROF_T0(t_m3);
-      clock = __dadd_rn(clock, c.dur);
-      energy = __dadd_rn(energy, c.energy);
-      flops = __dadd_rn(flops, c.flops);
-      bytes = __dadd_rn(bytes, c.bytes);
+      clock = __dadd_rn(clock, cd);
+      energy = __dadd_rn(energy, ce);
+      flops = __dadd_rn(flops, cf);
+      bytes = __dadd_rn(bytes, cb);
       max_batch = max_batch > B ? max_batch : int64_t(B);
       sum_batch += B;
       const int64_t n_new = n + 1;
@@ -737,64 +714,25 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       next_fin = m == kNoRel ? kNoFin : n + m;
       PROF_ADD(3, t_m3);
     } else {
-      PROF_CNT(11);
-      PROF_T0(t_d1);
       // ---- decode-only run: exact macro-stepping ----
-      Cost c;
-      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
-        c.dur = memo[4 * (B - 1)];
-        c.energy = memo[4 * (B - 1) + 1];
-        c.flops = memo[4 * (B - 1) + 2];
-        c.bytes = memo[4 * (B - 1) + 3];
-      } else {
-        PROF_CNT(12);
-        c = eval_iteration(pcs, cc, cv, p2p_slot, p2p_val, a.items, 0, B, B, qv, clampbits);
-        if (B <= p.memo_cap) {
-          if (lane == 0) {
-            memo[4 * (B - 1) + 1] = c.energy;
-            memo[4 * (B - 1) + 2] = c.flops;
-            memo[4 * (B - 1) + 3] = c.bytes;
-            memo[4 * (B - 1)] = c.dur;
-          }
-          __syncwarp();
-        }
-      }
-      const double d = c.dur, e = c.energy, f = c.flops, b = c.bytes;
-      PROF_ADD(4, t_d1);
       PROF_T0(t_d2);
-      // iterations until the first finish (inclusive)
+      // iterations until the first finish (inclusive), cut at the first KV
+      // overflow (batching.cpp:112): used + k*B > cap_tok
       int64_t kmax = next_fin - n;
-      // first k with (used + k*B)*kv > cap (batching.cpp:112 overflow)
-      if (!fits(used + kmax * int64_t(B))) {
-        const double r = (cap / kv - double(used)) / double(B);
-        int64_t k0 = r >= double(kmax) ? kmax - 1 : (r < 0.0 ? 0 : int64_t(floor(r)));
-        while (k0 > 0 && !fits(used + k0 * int64_t(B))) --k0;
-        while (k0 + 1 < kmax && fits(used + (k0 + 1) * int64_t(B))) ++k0;
-        kmax = k0 + 1;
-      }
+      if (used + kmax * int64_t(B) > cap_tok) kmax = (cap_tok - used) / B + 1;
       // Arrival event: only a not-yet-arrived head can change the batch; an
       // arrived head that admit() left in place stays blocked for the whole
       // run (used only grows, B is fixed).
       bool check = false, rej_h = false;
-      int64_t j_adm = -1;
       if (hd_valid && !hd_stack && hd_arr > clock) {
-        rej_h = __dmul_rn(double(hd_ctx), kv) > cap;
+        rej_h = hd_ctx > cap_tok;
         if (rej_h) {
           check = true;
-        } else if (!(max_bs > 0 && int64_t(B) >= max_bs) && fits(used + hd_ctx)) {
-          check = true;
-          // largest j in [0, kmax] with used + j*B + ctx fitting
-          if (fits(used + kmax * int64_t(B) + hd_ctx)) {
-            j_adm = kmax;
-          } else {
-            const double r = (cap / kv - double(used + hd_ctx)) / double(B);
-            int64_t j0 = r >= double(kmax) ? kmax - 1 : (r < 0.0 ? 0 : int64_t(floor(r)));
-            while (j0 > 0 && !fits(used + j0 * int64_t(B) + hd_ctx)) --j0;
-            while (j0 + 1 < kmax && fits(used + (j0 + 1) * int64_t(B) + hd_ctx)) ++j0;
-            j_adm = j0;
-          }
+        } else if (!(max_bs > 0 && int64_t(B) >= max_bs) && used + hd_ctx <= cap_tok) {
+          check = true;  // admissible at iteration start j while used + j*B + ctx fits
         }
       }
+      const double d = cd, e = ce, f = cf, b = cb;
       int64_t j = 0;
       bool stop = false;
       PROF_ADD(5, t_d2);
@@ -819,7 +757,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           bytes = __dadd_rn(bytes, b);
           ++j;
         }
-        if (j < kmax && (rej_h || j <= j_adm)) stop = true;
+        if (j < kmax && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) stop = true;
       }
       if (!stop) {
         for (; j + 4 <= kmax; j += 4) {
@@ -842,7 +780,76 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       if (j > 0) max_batch = max_batch > B ? max_batch : int64_t(B);
       settle = !stop;
     }
-    if (settle) finish_and_evict();
+    if (!settle) continue;
+
+    // ---- finish removal (batching.cpp:95-102) + metrics
+    // (simulator.cpp:143-156) at iteration n; finished slots become
+    // tombstones ----
+    PROF_T0(t_fin);
+    if (next_fin == n) {
+      PROF_CNT(13);
+      int64_t freed = 0;
+      unsigned m = kNoRel, nfin = 0;
+      for (int base = 0; base < len; base += kWarp) {
+        const int i = base + lane;
+        const int64_t fin = i < len ? a.fin[i] : kDead;
+        const bool fnow = fin == n;
+        unsigned tok = 0;
+        if (fnow) {
+          const int32_t gen = a.gen[i];
+          const double arr = a.arr[i], ft = a.ft[i];
+          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
+          const size_t s = slot_base + a.slot[i];
+          p.slot_e2e[s] = __dsub_rn(clock, arr);
+          p.slot_ttft[s] = __dsub_rn(ft, anchor);
+          p.slot_tpot[s] = gen >= 2 ? __ddiv_rn(__dsub_rn(clock, ft), double(gen - 1)) : 0.0;
+          p.slot_status[s] = 1;
+          a.fin[i] = kDead;
+          tok = unsigned(a.ctx[i] + gen);
+        }
+        freed += int64_t(__reduce_add_sync(kFull, tok));
+        nfin += __popc(__ballot_sync(kFull, fnow));
+        m = min(m, __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n)));
+      }
+      B -= int(nfin);
+      completed += nfin;
+      used -= freed;
+      next_fin = m == kNoRel ? kNoFin : n + m;
+      trim();
+      if (len > 2 * B + 2 * kWarp) compact();
+    }
+    PROF_ADD(7, t_fin);
+    // ---- LIFO eviction on overflow (batching.cpp:110-125) ----
+    PROF_T0(t_evi);
+    bool evicted = false;
+    while (B > 1 && used > cap_tok) {
+      const int i = len - 1;  // newest live request (trim invariant)
+      const int64_t fin = a.fin[i];
+      const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
+      used -= int64_t(a.ctx[i]) + tok;
+      if (fin == kNoFin) --n_pre;
+      if (lane == 0) {
+        g_stack[stack_top] = a.tidx[i];  // push_front of pending
+        a.fin[i] = kDead;
+      }
+      ++stack_top;
+      --B;
+      evicted = true;
+      trim();
+    }
+    if (B == 1 && used > cap_tok) {  // a lone outgrowing request is rejected
+      reject_slot(a.slot[len - 1]);
+      B = len = first_pre = n_pre = 0;
+      used = 0;
+      next_fin = kNoFin;
+      evicted = false;
+    }
+    __syncwarp();
+    if (evicted) {
+      load_head();
+      recompute_next_fin();
+    }
+    PROF_ADD(8, t_evi);
   }
 
   // ---- unit outputs ----
@@ -868,13 +875,11 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     o.pad = 0;
     p.uout[blockIdx.x] = o;
   }
-  const int nslots = pc.C + pc.K + ND;
-  for (int s = lane; s < nslots && s < kMaxClampSlots; s += kWarp) {
+  for (int s = lane; s < NQ; s += kWarp) {
     const uint32_t bits = clampbits[s];
-    if (!bits) continue;
-    const int t = s < pc.C ? cc[s].table : cv[s - pc.C].table;
-    if (t < 0) continue;
-    atomicOr((s < pc.C ? p.clamp_compute : p.clamp_curve) + t, bits);
+    const int t = desc[s].table;
+    if (!bits || t < 0) continue;
+    atomicOr((s < C ? p.clamp_compute : p.clamp_curve) + t, bits);
   }
 }
 
