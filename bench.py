@@ -162,26 +162,6 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------
 
-def lpt_shards(problems, freqs_of, ws):
-    """Longest-first assignment of (problem, entry) pairs to ranks; cost
-    estimate = requests per DP replica (the unit's serial chain length)."""
-    items = []
-    for pi, prob in enumerate(problems):
-        dp = list(prob.plans.struct.model_dp[i] for i in range(prob.plans.struct.n_plans))
-        F = max(1, len(freqs_of[pi]))
-        ntr = prob.trace.struct.n
-        for e in range(len(dp) * F):
-            items.append((ntr / dp[e // F], pi, e))
-    items.sort(key=lambda t: (-t[0], t[1], t[2]))
-    load = [0.0] * ws
-    shards = [[[] for _ in problems] for _ in range(ws)]
-    for cost, pi, e in items:
-        r = min(range(ws), key=lambda k: (load[k], k))
-        load[r] += cost
-        shards[r][pi].append(e)
-    return shards
-
-
 def load_profile_summary():
     p = os.path.join(REPO, "profiles", "sim_kernel_summary.json")
     if os.path.exists(p):
@@ -244,7 +224,9 @@ def main():
     problems = [problem_for(WORKLOADS[k]) for k in keys]
     freqs = [WORKLOADS[k].freqs for k in keys]
     objs = [WORKLOADS[k].objective for k in keys]
-    shards = lpt_shards(problems, freqs, ws)[rank] if ws > 1 else None
+    from paper_2411_17651_b200 import distributed as pdist
+    shards = (pdist.lpt_shards(pdist.entry_costs(problems, freqs), len(problems), ws)[rank]
+              if ws > 1 else None)
     flush = torch.empty(args.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
     def one_step():
@@ -268,35 +250,10 @@ def main():
             st["launches"] += res.gpu_launches
             st["entries"] += len(res)
             if ws > 1:
-                keys_np = np.zeros(len(res), dtype=[("num_rejected", "<i8"), ("objective_metric", "<f8"),
-                                                    ("other_metric", "<f8"), ("enc_rank", "<i4"),
-                                                    ("pad_", "<i4"), ("freq_ghz", "<f8"),
-                                                    ("entry_index", "<i8")])
-                lat = objs[pi] == "latency"
-                ent = res.entries
-                keys_np["num_rejected"] = ent["num_rejected"]
-                keys_np["objective_metric"] = ent["e2e_latency"] if lat else ent["total_energy"]
-                keys_np["other_metric"] = ent["total_energy"] if lat else ent["e2e_latency"]
-                enc = prob.plans.struct.enc_rank
-                keys_np["enc_rank"] = [enc[int(p)] for p in ent["plan_index"]]
-                keys_np["freq_ghz"] = ent["freq_ghz"]
-                keys_np["entry_index"] = ent["entry_index"]
-                st["best"].append((pi, keys_np))
-        if ws > 1:
-            import torch.distributed as dist
-            for pi, keys_np in st["best"]:
-                raw = torch.from_numpy(keys_np.view(np.uint8).copy()).to(dev)
-                n = torch.tensor([raw.numel()], device=dev)
-                sizes = [torch.zeros_like(n) for _ in range(ws)]
-                dist.all_gather(sizes, n)
-                mx = int(max(s.item() for s in sizes))
-                buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
-                buf[:raw.numel()] = raw
-                got = [torch.zeros_like(buf) for _ in range(ws)]
-                dist.all_gather(got, buf)
-                allk = np.concatenate([g[:int(s.item())].cpu().numpy() for g, s in zip(got, sizes)]
-                                      ).view(keys_np.dtype)
-                engine.rank_keys(allk)
+                st["best"].append(pdist.rank_keys_of(res, prob.plans.struct.enc_rank, objs[pi]))
+        if ws > 1:  # one all_gather of ranking records per design space, ranked on device
+            for keys_np in st["best"]:
+                engine.rank_keys(pdist.all_gather_keys(keys_np, device=dev))
                 st["launches"] += 1
         st["wall_ms"] = 1e3 * (time.perf_counter() - t0)
         return st

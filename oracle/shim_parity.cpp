@@ -1,0 +1,161 @@
+// shim_parity — TEST INFRASTRUCTURE.  Runs the reference's plansim::search
+// (oracle/_ref/libplansim_ref.a) and the drop-in plansim_gpu::search
+// (paper_2411_17651_b200/csrc/shim, over libpsg.so) on the SAME in-memory
+// reference objects and compares every RankedPlans field: ranked order, all
+// SimulationReport scalars (bit-exact; MFU/MBU within 1e-9 relative), every
+// per_request metric, rejected ids, and the store's clamp-warning set.
+//
+// usage: shim_parity --model F --cluster F (--profiles F | --synth-profiles X)
+//        (--trace F | --synth-trace a,b,c,d,rate,n,seed) [--objective energy]
+//        [--freqs a,b] [--batching chunked --chunk N] [--max-batch N]
+//        [--anchor admission] [--jobs N] [--drop-table OP]
+// Prints one JSON line; exit 0 on full parity, 1 on a mismatch, 3/4 when both
+// implementations raise the same InfeasibleError / DataError.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "plansim/simulator.hpp"
+#include "plansim_gpu.hpp"
+
+using namespace plansim;
+
+namespace {
+
+std::vector<double> doubles(const std::string& s) {
+  std::vector<double> v;
+  std::stringstream ss(s);
+  std::string t;
+  while (std::getline(ss, t, ',')) v.push_back(std::stod(t));
+  return v;
+}
+
+std::string drop_lines(const std::string& text, const std::string& needle) {
+  std::istringstream in(text);
+  std::ostringstream out;
+  std::string line;
+  while (std::getline(in, line))
+    if (line.find(needle) == std::string::npos) out << line << "\n";
+  return out.str();
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  std::string model_p, cluster_p, prof_p, trace_p, objective = "latency", drop;
+  double synth_ctx = 0;
+  std::vector<double> synth_tr, freqs;
+  SimConfig cfg;
+  int jobs = 1;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    const std::string k = argv[i], v = argv[i + 1];
+    if (k == "--model") model_p = v;
+    else if (k == "--cluster") cluster_p = v;
+    else if (k == "--profiles") prof_p = v;
+    else if (k == "--trace") trace_p = v;
+    else if (k == "--synth-profiles") synth_ctx = std::stod(v);
+    else if (k == "--synth-trace") synth_tr = doubles(v);
+    else if (k == "--objective") objective = v;
+    else if (k == "--freqs") freqs = doubles(v);
+    else if (k == "--batching") cfg.policy.mode = v == "chunked" ? BatchMode::ChunkedPrefill : BatchMode::Contiguous;
+    else if (k == "--chunk") cfg.policy.chunk_size = std::stoll(v);
+    else if (k == "--max-batch") cfg.policy.max_batch_size = std::stoll(v);
+    else if (k == "--anchor") cfg.ttft_anchor = v == "admission" ? TtftAnchor::Admission : TtftAnchor::Arrival;
+    else if (k == "--jobs") jobs = std::stoi(v);
+    else if (k == "--drop-table") drop = v;
+  }
+  try {
+    const ModelSpec model = parse_model_config_file(model_p);
+    const ClusterSpec cluster = parse_cluster_spec_file(cluster_p);
+    std::string store_text;
+    if (!prof_p.empty()) {
+      store_text = read_file(prof_p);
+    } else {
+      store_text = synth_profiles(cluster.device, cluster, GridSpec::for_model(model, cluster, synth_ctx)).serialize();
+    }
+    if (!drop.empty()) store_text = drop_lines(store_text, "\"op\":\"" + drop + "\"");
+    std::istringstream s1(store_text), s2(store_text);
+    const ProfileStore ref_store = ProfileStore::load(s1);
+    const ProfileStore gpu_store = ProfileStore::load(s2);
+    const Trace trace = !trace_p.empty() ? load_trace_file(trace_p)
+                                         : synth_trace({synth_tr[0], synth_tr[1]}, {synth_tr[2], synth_tr[3]},
+                                                       synth_tr[4], int64_t(synth_tr[5]), uint64_t(synth_tr[6]));
+    const auto plans = generate_plans(model, to_transformer_ir(model), cluster);
+    const Objective obj = objective == "energy" ? Objective::Energy : Objective::Latency;
+
+    int ref_code = 0, gpu_code = 0;
+    std::string ref_msg, gpu_msg;
+    RankedPlans a, b;
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+      a = search(plans, model, cluster, trace, ref_store, obj, freqs, cfg, jobs);
+    } catch (const InfeasibleError& e) { ref_code = 3; ref_msg = e.what(); }
+    catch (const DataError& e) { ref_code = 4; ref_msg = e.what(); }
+    const auto t1 = std::chrono::steady_clock::now();
+    try {
+      b = plansim_gpu::search(plans, model, cluster, trace, gpu_store, obj, freqs, cfg, jobs);
+    } catch (const InfeasibleError& e) { gpu_code = 3; gpu_msg = e.what(); }
+    catch (const DataError& e) { gpu_code = 4; gpu_msg = e.what(); }
+    const auto t2 = std::chrono::steady_clock::now();
+
+    if (ref_code || gpu_code) {
+      const bool same = ref_code == gpu_code && ref_msg == gpu_msg;
+      std::printf("{\"error_parity\":%s,\"ref\":\"%s\",\"gpu\":\"%s\"}\n", same ? "true" : "false",
+                  ref_msg.c_str(), gpu_msg.c_str());
+      return same ? ref_code : 1;
+    }
+    int bad = 0;
+    std::string first;
+    auto miss = [&](const std::string& what) {
+      if (!bad++) first = what;
+    };
+    if (a.entries.size() != b.entries.size()) miss("entry count");
+    for (size_t i = 0; i < a.entries.size() && i < b.entries.size(); ++i) {
+      const auto& x = a.entries[i];
+      const auto& y = b.entries[i];
+      const auto& r = x.report;
+      const auto& g = y.report;
+      const std::string at = " at rank " + std::to_string(i) + " " + r.plan_encoding;
+      if (x.plan_index != y.plan_index || x.freq_ghz != y.freq_ghz) miss("entry identity" + at);
+      if (r.plan_encoding != g.plan_encoding || r.frequency_ghz != g.frequency_ghz) miss("encoding" + at);
+      if (r.e2e_latency != g.e2e_latency || r.total_energy != g.total_energy ||
+          r.p95_latency != g.p95_latency || r.mean_ttft != g.mean_ttft || r.mean_tpot != g.mean_tpot)
+        miss("latency/energy/ttft/tpot" + at);
+      auto close = [](double u, double v) { return u == v || std::fabs(u - v) <= 1e-9 * std::fmax(std::fabs(u), std::fabs(v)); };
+      if (!close(r.mfu, g.mfu) || !close(r.mbu, g.mbu)) miss("mfu/mbu" + at);
+      if (r.num_completed != g.num_completed || r.num_rejected != g.num_rejected ||
+          r.num_iterations != g.num_iterations || r.max_batch_observed != g.max_batch_observed)
+        miss("counters" + at);
+      if (r.rejected_ids != g.rejected_ids) miss("rejected ids" + at);
+      if (r.per_request.size() != g.per_request.size()) {
+        miss("per_request size" + at);
+      } else {
+        for (size_t k = 0; k < r.per_request.size(); ++k) {
+          const auto& p = r.per_request[k];
+          const auto& q = g.per_request[k];
+          if (p.id != q.id || p.ttft != q.ttft || p.tpot != q.tpot || p.e2e != q.e2e || p.gen_len != q.gen_len) {
+            miss("per_request" + at);
+            break;
+          }
+        }
+      }
+    }
+    const auto wa = ref_store.warnings(), wb = gpu_store.warnings();
+    const std::set<std::string> sa(wa.begin(), wa.end()), sb(wb.begin(), wb.end());
+    if (sa != sb) miss("clamp warnings");
+    std::printf("{\"entries\":%zu,\"mismatches\":%d,\"first\":\"%s\",\"warnings\":%zu,"
+                "\"ref_s\":%.6f,\"gpu_s\":%.6f,\"best\":\"%s\"}\n",
+                a.entries.size(), bad, first.c_str(), sa.size(),
+                std::chrono::duration<double>(t1 - t0).count(),
+                std::chrono::duration<double>(t2 - t1).count(),
+                a.entries.empty() ? "" : a.entries.front().report.plan_encoding.c_str());
+    return bad ? 1 : 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 4;
+  }
+}

@@ -1,0 +1,36 @@
+// plansim_gpu.hpp — drop-in replacement for the reference's evaluate-all-plans
+// entry points, over the reference's own C++ types.  A plansim build adds
+// plansim_gpu.cpp and links libpsg.so; callers switch
+//     plansim::search(...)  ->  plansim_gpu::search(...)
+// (same arguments, same RankedPlans result, same exceptions).  See
+// INTEGRATION.md.
+//
+// Replaces: plansim::search        include/plansim/simulator.hpp:99-103
+//           plansim::simulate_plan include/plansim/simulator.hpp:80-82
+#pragma once
+
+#include <vector>
+
+#include "plansim/simulator.hpp"
+
+namespace plansim_gpu {
+
+// `jobs` is accepted for signature compatibility; the GPU is the worker pool.
+// `device` selects the CUDA device (one context per device is cached).
+plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
+                            const plansim::ModelSpec& model,
+                            const plansim::ClusterSpec& cluster,
+                            const plansim::Trace& trace,
+                            const plansim::ProfileStore& store,
+                            plansim::Objective objective,
+                            const std::vector<double>& frequencies,
+                            const plansim::SimConfig& cfg, int jobs = 1, int device = 0);
+
+plansim::SimulationReport simulate_plan(const plansim::ExecutionPlan& plan,
+                                        const plansim::ModelSpec& model,
+                                        const plansim::ClusterSpec& cluster,
+                                        const plansim::Trace& trace,
+                                        const plansim::ProfileStore& store,
+                                        const plansim::SimConfig& cfg, int device = 0);
+
+}  // namespace plansim_gpu

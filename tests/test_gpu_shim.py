@@ -1,0 +1,61 @@
+"""The drop-in boundary over the reference's own C++ types: plansim_gpu::search
+(paper_2411_17651_b200/csrc/shim) vs plansim::search, both called in one
+process (oracle/_ref/shim_parity) on the same ExecutionPlan / Trace /
+ProfileStore objects — ranked order, every SimulationReport field, per-request
+metrics, rejected ids, clamp warnings and exception parity."""
+import json
+import os
+import subprocess
+
+import pytest
+
+import pyoracle
+from paper_2411_17651_b200.workloads import WORKLOADS
+
+pytestmark = pytest.mark.gpu
+SHIM = os.path.join(os.path.dirname(pyoracle.REFDRV), "shim_parity")
+needs = pytest.mark.skipif(not os.path.exists(SHIM), reason="oracle/_ref/shim_parity not built")
+
+
+def run(args):
+    p = subprocess.run([SHIM] + [str(a) for a in args], capture_output=True, text=True, timeout=900)
+    line = next((json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")), None)
+    return p.returncode, line, p.stderr
+
+
+CASES = [
+    ("c1", []),
+    ("c4", ["--jobs", "4"]),
+    ("c4e", ["--jobs", "4"]),
+    ("c3", ["--batching", "chunked", "--chunk", "512", "--jobs", "4"]),
+    ("c1", ["--max-batch", "3", "--anchor", "admission"]),
+]
+
+
+@needs
+@pytest.mark.parametrize("key,extra", CASES, ids=[k + "".join(e) for k, e in CASES])
+def test_drop_in_search_matches_reference(workdir, key, extra):
+    w = WORKLOADS[key]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shim_" + key))) + extra
+    rc, line, err = run(args)
+    assert rc == 0, (line, err)
+    assert line["mismatches"] == 0
+
+
+@needs
+def test_drop_in_clamp_warnings_match(workdir):
+    # a 4096-token grid clamps every longer prompt: warnings must match
+    w = WORKLOADS["c1"]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shim_clamp")))
+    args[args.index("--synth-profiles") + 1] = "256"
+    rc, line, err = run(args)
+    assert rc == 0, (line, err)
+    assert line["warnings"] > 0
+
+
+@needs
+def test_drop_in_raises_the_reference_data_error(workdir):
+    w = WORKLOADS["c1"]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shim_err"))) + ["--drop-table", "gemm"]
+    rc, line, err = run(args)
+    assert rc == 4 and line["error_parity"], (line, err)
