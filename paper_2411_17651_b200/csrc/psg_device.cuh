@@ -90,9 +90,13 @@ struct SimParams {
   int32_t anchor;
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
-  int32_t tab_smem;          // doubles of per-unit table staging in shared memory (0: global)
-  int32_t tab_cap;           // doubles of table staging a unit may need
-  double* g_tab;             // global staging fallback, tab_cap doubles per unit
+  int32_t tab_smem;          // doubles of per-unit curve staging in shared memory
+  // precomputed cost tables (psg_tables.cu)
+  const int32_t* cell_sig;   // [n_freq_slots * n_cells_total] -> cell signature
+  const double* qtab;        // per signature, per token count: {t, e_raw, flops, bytes}
+  const int64_t* qoff;       // [n_sig] first row of the signature
+  const double* dectab;      // per local entry, per batch B >= 1: {dur, energy, flops, bytes}
+  const int64_t* doff;       // [entries] first row of the entry
   int64_t n_slots;           // requests per entry (== trace length)
   // outputs
   UnitOut* uout;
@@ -106,6 +110,32 @@ struct SimParams {
   unsigned long long* prof;  // PSG_PHASE_PROFILE builds: kProfSlots counters per unit
   int32_t* g_i32;            // kGI32 int32 arrays per unit, stride n_req
   double* g_f64;             // kGF64 8-byte arrays per unit, stride n_req
+};
+
+// Parameters of the cost-table kernels (psg_tables.cu).
+struct TabParams {
+  DPlans P;
+  DStore S;
+  // cell signatures: (compute grid, token_scale, tasks, width, op, shape)
+  int32_t n_sig;
+  const int32_t* sig_table;
+  const int32_t* sig_op;
+  const double *sig_scale, *sig_tasks, *sig_width, *sig_hidden, *sig_head, *sig_kv;
+  const int64_t* sig_rows;   // rows (token counts 0..rows-1) per signature
+  const int64_t* qoff;
+  double* qtab;
+  // decode tables per local entry
+  int32_t n_entries;
+  const int32_t* ent_plan;
+  const int32_t* ent_fslot;
+  const int64_t* ent_rows;   // Dmax per entry (B = 1..Dmax)
+  const int64_t* doff;
+  const int32_t* cell_sig;   // [n_freq_slots * n_cells_total]
+  int32_t n_cells_total;
+  const int32_t* coll_tab;
+  const int32_t* p2p_tab;
+  const int32_t* entry_missing;
+  double* dectab;
 };
 
 // ---------------------------------------------------------------------------
@@ -221,6 +251,53 @@ __device__ __forceinline__ void sample(const QDesc& d, const double* vals, const
   }
   sec = as;
   joule = aj;
+}
+
+// The reference's query_time + query_energy of one compute grid, literally
+// (cost.cpp:196-260: locate per axis, skip-zero-weight trilinear sum), reading
+// the store from global memory.  Used by the table kernels.
+__device__ __forceinline__ void cell_query_ref(const DStore& S, int table, double x, double tasks,
+                                               double width, double& sec, double& joule,
+                                               uint32_t& clamp) {
+  const int nc = S.c_n_ctx[table], nt = S.c_n_tasks[table], nw = S.c_n_width[table];
+  const double* kn = S.c_knots + S.c_knot_begin[table];
+  const double* vs = S.c_seconds + S.c_value_begin[table];
+  const double* vj = S.c_joules + S.c_value_begin[table];
+  const AxisPos pi = locate(kn, nc, x);
+  const AxisPos pj = locate(kn + nc, nt, tasks);
+  const AxisPos pk = locate(kn + nc + nt, nw, width);
+  clamp = uint32_t(pi.clamp < 0) | uint32_t(pi.clamp > 0) << 1 | uint32_t(pj.clamp < 0) << 2 |
+          uint32_t(pj.clamp > 0) << 3 | uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
+  double as = 0.0, aj = 0.0;
+  for (int ci = 0; ci < 2; ++ci) {
+    const double wi = ci ? pi.t : __dsub_rn(1.0, pi.t);
+    if (wi == 0.0) continue;
+    for (int cj = 0; cj < 2; ++cj) {
+      const double wj = cj ? pj.t : __dsub_rn(1.0, pj.t);
+      if (wj == 0.0) continue;
+      for (int ck = 0; ck < 2; ++ck) {
+        const double wk = ck ? pk.t : __dsub_rn(1.0, pk.t);
+        if (wk == 0.0) continue;
+        const int64_t idx = (int64_t(ci ? pi.hi : pi.lo) * nt + (cj ? pj.hi : pj.lo)) * nw +
+                            (ck ? pk.hi : pk.lo);
+        const double w = __dmul_rn(__dmul_rn(wi, wj), wk);
+        as = __dadd_rn(as, __dmul_rn(w, vs[idx]));
+        aj = __dadd_rn(aj, __dmul_rn(w, vj[idx]));
+      }
+    }
+  }
+  sec = as;
+  joule = aj;
+}
+
+// The reference's collective query (cost.cpp:262-291): (1-t)*s[lo] + t*s[hi].
+__device__ __forceinline__ void curve_query_ref(const DStore& S, int curve, double x, double& sec,
+                                                double& joule) {
+  const int64_t b = S.k_begin[curve];
+  const AxisPos p = locate(S.k_payload + b, S.k_n[curve], x);
+  const double u = __dsub_rn(1.0, p.t);
+  sec = __dadd_rn(__dmul_rn(u, S.k_seconds[b + p.lo]), __dmul_rn(p.t, S.k_seconds[b + p.hi]));
+  joule = __dadd_rn(__dmul_rn(u, S.k_joules[b + p.lo]), __dmul_rn(p.t, S.k_joules[b + p.hi]));
 }
 
 // op_flops / op_bytes (cost.cpp:51-68), written in the reference's order.

@@ -125,7 +125,7 @@ struct psg_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
-  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj, d_tab, d_prof;
+  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
@@ -175,7 +175,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
-                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_tab, &ctx->d_prof})
+                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj}) b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -416,6 +416,86 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     entry_enc[e] = P->enc_rank[p];
   }
 
+  // ---- cell signatures and cost-table sizes (psg_tables.cu) ----
+  // A cell query depends only on (grid, token_scale, tasks, width, op, op
+  // shape) and the token count; plans sharing those share one table.
+  int64_t item_max = 0;
+  for (int64_t i = 0; i < N; ++i) item_max = std::max<int64_t>(item_max, T->context_len[i]);
+  if (cfg->batch_mode == PSG_BATCH_CHUNKED && cfg->chunk_size >= 1)
+    item_max = std::min<int64_t>(item_max, cfg->chunk_size);
+  std::vector<int64_t> ent_rows(E, 1);  // decode tables cover B = 1..max replica size
+  for (const auto& u : units) ent_rows[u.entry] = std::max<int64_t>(ent_rows[u.entry], u.n_req);
+  auto fbits = [](double v) {
+    uint64_t b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+  };
+  std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t>, int> sig_of;
+  std::vector<int32_t> sig_table, sig_op, cell_sig(std::max<size_t>(size_t(F) * n_cells, 1), 0);
+  std::vector<double> sig_scale, sig_tasks, sig_width, sig_hidden, sig_head, sig_kv;
+  std::vector<int64_t> sig_rows;
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F), f = int(ent[e] % F);
+    for (int c = P->cell_begin[p]; c < P->cell_begin[p + 1]; ++c) {
+      const int t = cell_tab[size_t(f) * n_cells + c];
+      const auto key = std::make_tuple(t, P->cell_op[c], fbits(P->cell_token_scale[c]),
+                                       fbits(P->cell_tasks[c]), fbits(P->cell_width[c]),
+                                       fbits(P->shape_hidden[p]), fbits(P->shape_head_dim[p]),
+                                       fbits(P->shape_kv_elems[p]));
+      auto it = sig_of.find(key);
+      int sg;
+      if (it == sig_of.end()) {
+        sg = int(sig_table.size());
+        sig_of.emplace(key, sg);
+        sig_table.push_back(t);
+        sig_op.push_back(P->cell_op[c]);
+        sig_scale.push_back(P->cell_token_scale[c]);
+        sig_tasks.push_back(P->cell_tasks[c]);
+        sig_width.push_back(P->cell_width[c]);
+        sig_hidden.push_back(P->shape_hidden[p]);
+        sig_head.push_back(P->shape_head_dim[p]);
+        sig_kv.push_back(P->shape_kv_elems[p]);
+        sig_rows.push_back(1);
+      } else {
+        sg = it->second;
+      }
+      cell_sig[size_t(f) * n_cells + c] = sg;
+      sig_rows[sg] = std::max<int64_t>(sig_rows[sg], std::max(item_max, ent_rows[e]) + 1);
+    }
+  }
+  const int n_sig = int(sig_table.size());
+  std::vector<int64_t> qoff(std::max(n_sig, 1), 0), doff(std::max(E, 1), 0);
+  int64_t qrows = 0, drows = 0, max_qrows = 1, max_drows = 1;
+  for (int g = 0; g < n_sig; ++g) {
+    qoff[g] = qrows;
+    qrows += sig_rows[g];
+    max_qrows = std::max(max_qrows, sig_rows[g]);
+  }
+  std::vector<int32_t> ent_plan(std::max(E, 1)), ent_fslot(std::max(E, 1));
+  for (int e = 0; e < E; ++e) {
+    doff[e] = drows;
+    drows += ent_rows[e];
+    max_drows = std::max(max_drows, ent_rows[e]);
+    ent_plan[e] = int32_t(ent[e] / F);
+    ent_fslot[e] = int32_t(ent[e] % F);
+  }
+  if (max_qrows > int64_t(65535) * 256 || max_drows > int64_t(65535) * 256)
+    return fail(ctx, PSG_ERR_USAGE, "trace too long for the cost-table grid");
+  // curves staged per unit in shared memory
+  size_t tab_cap = 1;
+  for (int e = 0; e < E; ++e) {
+    const int p = int(ent[e] / F);
+    size_t need = 0;
+    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1]; ++k)
+      need += 3 * size_t(coll_tab[k] >= 0 ? S->k_n[coll_tab[k]] : 1);
+    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b)
+      need += 3 * size_t(p2p_tab[b] >= 0 ? S->k_n[p2p_tab[b]] : 1);
+    tab_cap = std::max(tab_cap, need);
+  }
+  if (tab_cap * sizeof(double) > 96 * 1024)
+    return fail(ctx, PSG_ERR_USAGE, "collective curves of one plan exceed on-chip staging (96 KB)");
+  const int tab_smem = int(tab_cap);
+
   // ---- pack inputs ----
   Packer pk;
   const size_t o_model_dp = pk.add(P->model_dp, np), o_stages = pk.add(P->num_stages, np),
@@ -458,6 +538,20 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
                o_eu = pk.add(entry_units.data(), entry_units.size()),
                o_epeak = pk.add(entry_peak.data(), E), o_eenc = pk.add(entry_enc.data(), E),
                o_efreq = pk.add(entry_freq.data(), E), o_eglob = pk.add(ent.data(), E);
+  const size_t o_sgt = pk.add(sig_table.data(), sig_table.size()),
+               o_sgo = pk.add(sig_op.data(), sig_op.size()),
+               o_sgs = pk.add(sig_scale.data(), sig_scale.size()),
+               o_sgk = pk.add(sig_tasks.data(), sig_tasks.size()),
+               o_sgw = pk.add(sig_width.data(), sig_width.size()),
+               o_sgh = pk.add(sig_hidden.data(), sig_hidden.size()),
+               o_sghd = pk.add(sig_head.data(), sig_head.size()),
+               o_sgkv = pk.add(sig_kv.data(), sig_kv.size()),
+               o_sgr = pk.add(sig_rows.data(), sig_rows.size()), o_qoff = pk.add(qoff.data(), qoff.size()),
+               o_csig = pk.add(cell_sig.data(), cell_sig.size()),
+               o_eplan = pk.add(ent_plan.data(), ent_plan.size()),
+               o_efs = pk.add(ent_fslot.data(), ent_fslot.size()),
+               o_erows = pk.add(ent_rows.data(), ent_rows.size()),
+               o_doff = pk.add(doff.data(), doff.size());
   const size_t in_bytes = pk.size;
 
   // ---- device buffers ----
@@ -468,25 +562,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(ctx->d_slot_u8.ensure(std::max<size_t>(slots, 1)));
   PSG_CUDA(ctx->d_scratch_i32.ensure(std::max<int64_t>(scratch_total, 1) * kScratchI32 * sizeof(int32_t)));
   PSG_CUDA(ctx->d_scratch_f64.ensure(std::max<int64_t>(scratch_total, 1) * kScratchF64 * sizeof(double)));
-  // per-unit table staging: shared memory when it fits, else a global region
-  size_t tab_cap = 1;
-  for (int e = 0; e < E; ++e) {
-    const int p = int(ent[e] / F), f = int(ent[e] % F);
-    std::vector<int> nctx, ncurve;
-    for (int c = P->cell_begin[p]; c < P->cell_begin[p + 1]; ++c) {
-      const int t = cell_tab[size_t(f) * n_cells + c];
-      nctx.push_back(t >= 0 ? S->c_n_ctx[t] : 1);
-    }
-    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1]; ++k)
-      ncurve.push_back(coll_tab[k] >= 0 ? S->k_n[coll_tab[k]] : 1);
-    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b)
-      ncurve.push_back(p2p_tab[b] >= 0 ? S->k_n[p2p_tab[b]] : 1);
-    tab_cap = std::max(tab_cap, sim_tab_doubles(int(nctx.size()), nctx.data(), int(ncurve.size()),
-                                                ncurve.data()));
-  }
-  if (tab_cap * sizeof(double) > 96 * 1024)
-    return fail(ctx, PSG_ERR_USAGE, "profile tables of one plan exceed on-chip staging (96 KB)");
-  const int tab_smem = int(tab_cap);
+  PSG_CUDA(ctx->d_qtab.ensure(size_t(std::max<int64_t>(qrows, 1)) * 4 * sizeof(double)));
+  PSG_CUDA(ctx->d_dtab.ensure(size_t(std::max<int64_t>(drows, 1)) * 4 * sizeof(double)));
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
   Packer wk;  // offsets only
   const size_t w_uout = wk.add<UnitOut>(nullptr, n_units), w_eout = wk.add<EntryOut>(nullptr, E),
@@ -537,8 +614,38 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.smem_cap = 256;
   sp.memo_cap = 256;
   sp.tab_smem = tab_smem;
-  sp.tab_cap = int(tab_cap);
-  sp.g_tab = static_cast<double*>(ctx->d_tab.p);
+  sp.cell_sig = (const int32_t*)D(o_csig);
+  sp.qtab = static_cast<const double*>(ctx->d_qtab.p);
+  sp.qoff = (const int64_t*)D(o_qoff);
+  sp.dectab = static_cast<const double*>(ctx->d_dtab.p);
+  sp.doff = (const int64_t*)D(o_doff);
+
+  TabParams tp{};
+  tp.P = sp.P;
+  tp.S = sp.S;
+  tp.n_sig = n_sig;
+  tp.sig_table = (const int32_t*)D(o_sgt);
+  tp.sig_op = (const int32_t*)D(o_sgo);
+  tp.sig_scale = (const double*)D(o_sgs);
+  tp.sig_tasks = (const double*)D(o_sgk);
+  tp.sig_width = (const double*)D(o_sgw);
+  tp.sig_hidden = (const double*)D(o_sgh);
+  tp.sig_head = (const double*)D(o_sghd);
+  tp.sig_kv = (const double*)D(o_sgkv);
+  tp.sig_rows = (const int64_t*)D(o_sgr);
+  tp.qoff = sp.qoff;
+  tp.qtab = static_cast<double*>(ctx->d_qtab.p);
+  tp.n_entries = E;
+  tp.ent_plan = (const int32_t*)D(o_eplan);
+  tp.ent_fslot = (const int32_t*)D(o_efs);
+  tp.ent_rows = (const int64_t*)D(o_erows);
+  tp.doff = sp.doff;
+  tp.cell_sig = sp.cell_sig;
+  tp.n_cells_total = n_cells;
+  tp.coll_tab = sp.coll_tab;
+  tp.p2p_tab = sp.p2p_tab;
+  tp.entry_missing = sp.entry_missing;
+  tp.dectab = static_cast<double*>(ctx->d_dtab.p);
   sp.n_slots = N;
   sp.uout = (UnitOut*)W(w_uout);
   double* slot_f = static_cast<double*>(ctx->d_slot_f64.p);
@@ -589,6 +696,14 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
   const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem);
   PSG_CUDA(cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (n_sig > 0) {  // cell-query tables, then decode-only iteration tables
+    qtab_kernel<<<dim3(unsigned(n_sig), unsigned((max_qrows + 255) / 256)), 256, 0, st>>>(tp);
+    ++launches;
+  }
+  if (E > 0) {
+    dectab_kernel<<<dim3(unsigned(E), unsigned((max_drows + 255) / 256)), 256, 0, st>>>(tp);
+    ++launches;
+  }
   if (n_units > 0) {
     sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
     ++launches;

@@ -8,24 +8,26 @@
 //  * Scalar state is warp-uniform (every lane holds the same clock/energy),
 //    so there is no broadcast; batch scans are lane-parallel over the active
 //    slots with ballot/popc and REDUX reductions.
+//  * Cell queries are table lookups: psg_tables.cu tabulates every cell
+//    signature over token counts and every entry's decode-only iteration cost
+//    over batch sizes in parallel before this kernel runs.  The serial path
+//    only prices collectives (curves staged in shared memory) and performs
+//    the reference-ordered adds.
 //  * Shared memory holds everything an event touches: the active slots
 //    (SoA, tombstoned, migrating to a global region only if the batch
 //    outgrows them), a 32-request prefetch window of the replica's arrivals,
-//    the decode-cost memo, and the unit's cost tables — every cell's compute
-//    grid collapsed to its fixed (tasks, width) corners, every collective and
-//    distinct p2p curve — staged once at unit start.
+//    a decode-cost memo, and the unit's collective curves.
 //  * The KV ledger is an exact integer: cap_tok = max{T : double(T)*kv <= cap}
 //    turns every admission / overflow / admissibility test into an integer
-//    compare and every event horizon into one integer division.
+//    compare.
 //  * Exact event-driven macro-stepping: a decode-only iteration's workload is
 //    {decode_count = B}, so its (seconds, joules, flops, bytes) are bit-
 //    identical until the batch changes.  Between events (arrival of an
 //    admissible/rejectable head, first finish, first KV overflow) the unit
 //    runs a tight loop of the reference's sequential FP64 adds only.
-//  * Cost queries of one iteration run one per lane through a single
-//    divergence-free path (cells and curves share locate + sample); their
-//    accumulation is serial in the reference's order (cells -> items in
-//    admission order -> decode, collectives, then per-stage p2p).
+//  * Clamp warnings (cost.cpp:204-212, :273-278) are monotone in the token
+//    count, so the unit tracks the extreme token counts / totals it queried
+//    and derives the per-table flags once at the end.
 #include <climits>
 
 #include "psg_device.cuh"
@@ -41,9 +43,9 @@ constexpr int kGI32 = 7;  // global fallback arrays: stack, tidx, ctx, gen, done
 constexpr int kGF64 = 4;  // adm, ft, arr, fin
 
 // Phase profiler (dev builds only: -DPSG_PHASE_PROFILE; zero code otherwise).
-// slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 unused,
+// slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 decode cost,
 // 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
-// 11 #decode runs, 12 #decode evals, 13 #finish events, 14 unused, 15 total.
+// 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 -, 15 total.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -64,22 +66,27 @@ struct ActiveList {
   double *adm, *ft, *arr;
 };
 
+// A collective / p2p curve staged in shared memory (cost.cpp:262-291).
+struct CurveDesc {
+  int kn_off, n, table, pad;
+  double ppt, share, emul;  // payload = (ppt * tokens) * share; energy * emul
+};
+
 __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct SmemLayout {
-  size_t qv, desc, p2p_slot, p2p_val, combo, clamp, win_arr, win_i32, memo, act_f64, act_fin,
-      act_i32, tab, total;
+  size_t qv, cdesc, cellq, p2p_slot, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
+      tab, total;
 };
 
 __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem) {
   SmemLayout L;
   size_t o = 0;
   L.qv = o;        o = al16(o + sizeof(double) * 4 * kWarp);
-  L.desc = o;      o = al16(o + sizeof(QDesc) * kMaxClampSlots);
+  L.cdesc = o;     o = al16(o + sizeof(CurveDesc) * kMaxClampSlots);
+  L.cellq = o;     o = al16(o + sizeof(int64_t) * kMaxCells);
   L.p2p_slot = o;  o = al16(o + kMaxClampSlots);
   L.p2p_val = o;   o = al16(o + sizeof(double) * 2 * kMaxClampSlots);
-  L.combo = o;     o = al16(o + sizeof(int32_t) * kMaxCells * kMaxCombos);
-  L.clamp = o;     o = al16(o + sizeof(uint32_t) * kMaxClampSlots);
   L.win_arr = o;   o = al16(o + sizeof(double) * kWindow);
   L.win_i32 = o;   o = al16(o + sizeof(int32_t) * 4 * kWindow);
   L.memo = o;      o = al16(o + sizeof(double) * 4 * size_t(memo_cap));
@@ -118,11 +125,10 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem);
   double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
-  QDesc* desc = reinterpret_cast<QDesc*>(smem_raw + L.desc);
+  CurveDesc* cdesc = reinterpret_cast<CurveDesc*>(smem_raw + L.cdesc);
+  int64_t* cellq = reinterpret_cast<int64_t*>(smem_raw + L.cellq);  // qtab row 0 of each cell
   uint8_t* p2p_slot = reinterpret_cast<uint8_t*>(smem_raw + L.p2p_slot);
   double* p2p_val = reinterpret_cast<double*>(smem_raw + L.p2p_val);
-  int32_t* combo = reinterpret_cast<int32_t*>(smem_raw + L.combo);
-  uint32_t* clampbits = reinterpret_cast<uint32_t*>(smem_raw + L.clamp);
   double* w_arr = reinterpret_cast<double*>(smem_raw + L.win_arr);
   int32_t* w_i32 = reinterpret_cast<int32_t*>(smem_raw + L.win_i32);  // tidx, ctx, gen, slot
   double* memo = reinterpret_cast<double*>(smem_raw + L.memo);
@@ -136,11 +142,12 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   const double sdd = double(p.P.stage_devices[pl]);
   const double Sd = double(S);
   const double p2p_ppt = p.P.p2p_ppt[pl];
-  const double hidden = p.P.sh_hidden[pl], head_dim = p.P.sh_head[pl], kv_elems = p.P.sh_kv[pl];
   const int c0 = p.P.cell_begin[pl], C = p.P.cell_begin[pl + 1] - c0;
   const int k0 = p.P.coll_begin[pl], K = p.P.coll_begin[pl + 1] - k0;
   const int b0 = p.P.p2p_begin[pl], NB = p.P.p2p_begin[pl + 1] - b0;
   const int64_t cap_tok = ledger_cap_tokens(kv, cap);
+  const double* qtab = p.qtab;
+  const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
 
   // distinct p2p tables: boundaries only span 1 or 2 nodes in practice
   int ND = 0;
@@ -148,123 +155,62 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     const int t = p.p2p_tab[b0 + b];
     int s = 0;
     for (; s < ND; ++s)
-      if (desc[C + K + s].table == t) break;
+      if (cdesc[K + s].table == t) break;
     if (s == ND) {
-      if (lane == 0) desc[C + K + ND].table = t;
+      if (lane == 0) cdesc[K + ND].table = t;
       ++ND;
       __syncwarp();
     }
     if (lane == 0) p2p_slot[b] = uint8_t(s);
   }
-  const int NQ = C + K + ND;  // descriptors: cells, collectives, distinct p2p
-  uint64_t p2p_mask = 0;      // ND <= 2: bit b = distinct-table slot of boundary b
+  const int NQ = K + ND;  // curves: collectives, then distinct p2p
+  uint64_t p2p_mask = 0;  // ND <= 2: bit b = distinct-curve slot of boundary b
   __syncwarp();
   for (int b = 0; b < NB && ND <= 2; ++b) p2p_mask |= uint64_t(p2p_slot[b]) << b;
-  for (int s = lane; s < kMaxClampSlots; s += kWarp) {
-    clampbits[s] = 0;
-  }
   for (int i = lane; i < 4 * p.memo_cap; i += kWarp) memo[i] = -1.0;
-  __syncwarp();
-
-  // ---- stage the unit's tables (QDesc + values in shared memory) ----
+  if (lane < C) {
+    const int sig = p.cell_sig[size_t(U.fslot) * p.n_cells_total + c0 + lane];
+    cellq[lane] = p.qoff[sig];
+  }
   if (lane < NQ) {
-    QDesc d;
-    d.ncombo = 1;
-    d.wj[0] = d.wk[0] = 1.0;
-    d.clamp_tw = 0;
-    d.tasks = d.width = 0.0;
-    d.op = 0;
-    if (lane < C) {
-      const int g = c0 + lane;
-      d.is_cell = 1;
-      d.table = p.cell_tab[size_t(U.fslot) * p.n_cells_total + g];
-      d.op = p.P.cell_op[g];
-      d.tasks = p.P.cell_tasks[g];
-      d.width = p.P.cell_width[g];
-      d.scale = p.P.cell_scale[g];
-      d.share = 1.0;
-      d.emul = sdd;  // query_energy * stage_devices
-      d.n = 1;
-      d.ncombo = 0;
-      if (d.table >= 0) {
-        d.n = p.S.c_n_ctx[d.table];
-        const int nt = p.S.c_n_tasks[d.table], nw = p.S.c_n_width[d.table];
-        const double* kn = p.S.c_knots + p.S.c_knot_begin[d.table];
-        const AxisPos pj = locate(kn + d.n, nt, d.tasks);
-        const AxisPos pk = locate(kn + d.n + nt, nw, d.width);
-        d.clamp_tw = uint32_t(pj.clamp < 0) << 2 | uint32_t(pj.clamp > 0) << 3 |
-                     uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
-        for (int cj = 0; cj < 2; ++cj) {
-          const double wj = cj ? pj.t : __dsub_rn(1.0, pj.t);
-          if (wj == 0.0) continue;
-          for (int ck = 0; ck < 2; ++ck) {
-            const double wk = ck ? pk.t : __dsub_rn(1.0, pk.t);
-            if (wk == 0.0) continue;
-            d.wj[d.ncombo] = wj;
-            d.wk[d.ncombo] = wk;
-            combo[lane * kMaxCombos + d.ncombo] = (cj ? pj.hi : pj.lo) * nw + (ck ? pk.hi : pk.lo);
-            ++d.ncombo;
-          }
-        }
-      }
+    CurveDesc d;
+    if (lane < K) {
+      const int g = k0 + lane;
+      d.table = p.coll_tab[g];
+      d.ppt = p.P.coll_ppt[g];
+      d.share = p.P.coll_share[g];
+      d.emul = double(p.P.coll_groups[g]);  // query_energy * groups_per_stage
     } else {
-      d.is_cell = 0;
-      if (lane < C + K) {
-        const int g = k0 + lane - C;
-        d.table = p.coll_tab[g];
-        d.scale = p.P.coll_ppt[g];
-        d.share = p.P.coll_share[g];
-        d.emul = double(p.P.coll_groups[g]);  // query_energy * groups_per_stage
-      } else {
-        d.table = desc[lane].table;
-        d.scale = p2p_ppt;  // payload = p2p_ppt * tokens; x * 1.0 is exact
-        d.share = 1.0;
-        d.emul = 1.0;
-      }
-      d.n = d.table >= 0 ? p.S.k_n[d.table] : 1;
+      d.table = cdesc[lane].table;
+      d.ppt = p2p_ppt;  // payload = p2p_ppt * tokens; x * 1.0 is exact
+      d.share = 1.0;
+      d.emul = 1.0;
     }
-    desc[lane] = d;
+    d.n = d.table >= 0 ? p.S.k_n[d.table] : 1;
+    d.pad = 0;
+    cdesc[lane] = d;
   }
   __syncwarp();
-  {
+  {  // stage the curves: knots[n] then (seconds, joules)[n] interleaved
     int off = 0;
     for (int q = 0; q < NQ; ++q) {
-      const int n = desc[q].n, nc = desc[q].ncombo, t = desc[q].table;
+      const int n = cdesc[q].n, t = cdesc[q].table;
       double* kd = tab + off;
-      double* vd = kd + n;
       if (t >= 0) {
-        if (q < C) {
-          const double* kn = p.S.c_knots + p.S.c_knot_begin[t];
-          const double* vs = p.S.c_seconds + p.S.c_value_begin[t];
-          const double* vj = p.S.c_joules + p.S.c_value_begin[t];
-          const int plane = p.S.c_n_tasks[t] * p.S.c_n_width[t];
-          for (int i = lane; i < n; i += kWarp) kd[i] = kn[i];
-          for (int i = lane; i < n * nc; i += kWarp) {
-            const int r = i / nc, cb = i - r * nc;
-            const int64_t v = int64_t(r) * plane + combo[q * kMaxCombos + cb];
-            vd[2 * i] = vs[v];
-            vd[2 * i + 1] = vj[v];
-          }
-        } else {
-          const int64_t b = p.S.k_begin[t];
-          for (int i = lane; i < n; i += kWarp) {
-            kd[i] = p.S.k_payload[b + i];
-            vd[2 * i] = p.S.k_seconds[b + i];
-            vd[2 * i + 1] = p.S.k_joules[b + i];
-          }
+        const int64_t b = p.S.k_begin[t];
+        for (int i = lane; i < n; i += kWarp) {
+          kd[i] = p.S.k_payload[b + i];
+          kd[n + 2 * i] = p.S.k_seconds[b + i];
+          kd[n + 2 * i + 1] = p.S.k_joules[b + i];
         }
       }
-      if (lane == 0) {
-        desc[q].kn_off = off;
-        desc[q].val_off = off + n;
-      }
-      off += n * (1 + 2 * nc);
+      if (lane == 0) cdesc[q].kn_off = off;
+      off += 3 * n;
     }
   }
+  int n_curve_knots = 1;  // longest payload axis among the unit's curves
+  for (int q = 0; q < NQ; ++q) n_curve_knots = max(n_curve_knots, cdesc[q].n);
   __syncwarp();
-
-  int n_knots_max = 1;  // longest knot axis among the unit's tables
-  for (int q = 0; q < NQ; ++q) n_knots_max = max(n_knots_max, desc[q].n);
 
   // ---- active slots ----
   int cap_now = p.smem_cap;
@@ -309,6 +255,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated) <= cap_tok
   int64_t next_fin = kNoFin;
   int err = 0;
+  // extreme cell-query token counts and iteration totals (clamp reporting)
+  int64_t tok_lo = INT64_MAX, tok_hi = -1, tot_lo = INT64_MAX, tot_hi = -1;
 
   // pending head (batching.hpp:93 pending_.front()), warp-uniform registers
   bool hd_valid = false, hd_stack = false;
@@ -338,6 +286,11 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
         w_i32[kWindow + lane] = int(p.T.ctx[t]);
         w_i32[2 * kWindow + lane] = int(p.T.gen[t]);
         w_i32[3 * kWindow + lane] = p.T.slot[t];
+        // warm L1 with the cell rows this request's prefill will read
+        int64_t first = p.T.ctx[t];
+        if (chunked && chunk >= 1 && first > chunk) first = chunk;
+        for (int c = 0; c < C; ++c)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(qtab + (cellq[c] + first) * 4));
       }
       __syncwarp();
       PROF_ADD(9, t_ref);
@@ -496,15 +449,15 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     if (chunk_err) { err = 1; break; }
     if (missing) { err = 2; break; }
 
-    // ---- the iteration's workload (batching.cpp:67-76) ----
-    const bool mixed = n_pre > 0;
-    int n_items = 0;
-    int64_t pre_tok = 0;
-    double cd = 0.0, ce = 0.0, cf = 0.0, cb = 0.0;  // duration, energy, flops, bytes
-    bool need_eval = true;
-    if (mixed) {
+    bool settle = true;
+    if (n_pre > 0) {
+      // ---- mixed iteration (batching.cpp:62-108): prefill items from the
+      // prefill frontier, decode count = the rest ----
       PROF_CNT(10);
       PROF_T0(t_m1);
+      int n_items = 0;
+      int64_t pre_tok = 0;
+      unsigned it_lo = 0xffffffffu, it_hi = 0;
       for (int base = first_pre; base < len; base += kWarp) {
         const int i = base + lane;
         const bool pre = i < len && a.fin[i] == kNoFin;
@@ -518,85 +471,76 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
         if (pre) a.items[n_items + __popc(pm & lt_mask)] = tok;
         n_items += __popc(pm);
         pre_tok += __reduce_add_sync(kFull, unsigned(tok));
+        it_lo = min(it_lo, __reduce_min_sync(kFull, pre ? unsigned(tok) : 0xffffffffu));
+        it_hi = max(it_hi, __reduce_max_sync(kFull, pre ? unsigned(tok) : 0u));
       }
       __syncwarp();
-      PROF_ADD(1, t_m1);
-    } else {
-      PROF_CNT(11);
-      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
-        cd = memo[4 * (B - 1)];
-        ce = memo[4 * (B - 1) + 1];
-        cf = memo[4 * (B - 1) + 2];
-        cb = memo[4 * (B - 1) + 3];
-        need_eval = false;
-      } else {
-        PROF_CNT(12);
+      const int64_t decode = int64_t(B) - n_items;
+      const int64_t total = decode + pre_tok;
+      tok_lo = min(tok_lo, int64_t(it_lo));
+      tok_hi = max(tok_hi, int64_t(it_hi));
+      if (decode > 0) {
+        tok_lo = min(tok_lo, decode);
+        tok_hi = max(tok_hi, decode);
       }
-    }
-    const int64_t decode = int64_t(B) - n_items;
+      tot_lo = min(tot_lo, total);
+      tot_hi = max(tot_hi, total);
+      PROF_ADD(1, t_m1);
 
-    if (need_eval) {
       // ---- iteration_time (simulator.cpp:17-87) ----
       PROF_T0(t_ev);
       const int nq_c = n_items + (decode > 0 ? 1 : 0);
       const int Qc = C * nq_c;
-      const int Q = Qc + K + ND;
-      const double total_d = double(decode + pre_tok);
+      const int Q = Qc + NQ;
+      const double total_d = double(total);
       double bs = 0.0, bj = 0.0, bf = 0.0, bb = 0.0;
       for (int base = 0; base < Q; base += kWarp) {
         const int q = base + lane;
-        {
-          // Convergent straight-line query: every lane runs the same code
-          // (selects instead of branches); lanes past Q compute a dummy.
-          const bool act = q < Q;
-          const bool cellq = q < Qc;
-          const int cdi = cellq ? q / nq_c : 0;
-          const int item = q - cdi * nq_c;
-          const int di = act ? (cellq ? cdi : C + (q - Qc)) : 0;
-          const int64_t tok =
-              (cellq && item < n_items) ? int64_t(a.items[cellq ? item : 0]) : decode;
-          const QDesc& d = desc[di];
-          // cell: tokens * token_scale; curve: (ppt * tokens) * share
-          const double xc = __dmul_rn(double(tok), d.scale);
-          const double xk = __dmul_rn(__dmul_rn(d.scale, total_d), d.share);
-          const double x = d.is_cell ? xc : xk;
-          // locate (cost.cpp:85-102) by counting knots <= x: no data-
-          // dependent branches, independent loads
+        // cell query = one precomputed row {t, e_raw, flops, bytes}: issue the
+        // loads first so their latency overlaps the curve lanes' work
+        const bool cell_lane = q < Qc;
+        double2 te = make_double2(0.0, 0.0), fb = make_double2(0.0, 0.0);
+        if (cell_lane) {
+          const int c = q / nq_c;
+          const int i = q - c * nq_c;
+          const int64_t tok = i < n_items ? int64_t(a.items[i]) : decode;
+          const double2* row = reinterpret_cast<const double2*>(qtab + (cellq[c] + tok) * 4);
+          te = __ldg(row);
+          fb = __ldg(row + 1);
+        }
+        if (!cell_lane && q < Q) {
+          // collective / p2p curve query on the staged curve
+          const int k = q - Qc;
+          const CurveDesc& d = cdesc[k];
+          const double x = __dmul_rn(__dmul_rn(d.ppt, total_d), d.share);
           const double* kn = tab + d.kn_off;
-          const int n = d.n;
+          const int cn = d.n;
           int cnt = 0;
-          for (int j = 0; j < n_knots_max; ++j) {
-            const double kj = kn[j < n ? j : n - 1];
-            cnt += (j < n && kj <= x) ? 1 : 0;
+          for (int j = 0; j < n_curve_knots; ++j)
+            cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
+          const bool lo_c = x <= kn[0], hi_c = x >= kn[cn - 1];
+          const int lo = lo_c ? 0 : (hi_c ? cn - 1 : cnt - 1);
+          const int hi = lo_c ? 0 : (hi_c ? cn - 1 : cnt);
+          const bool interior = !(lo_c || hi_c);
+          const double t = __ddiv_rn(interior ? __dsub_rn(x, kn[lo]) : 0.0,
+                                     interior ? __dsub_rn(kn[hi], kn[lo]) : 1.0);
+          const double u = __dsub_rn(1.0, t);
+          const double* v = kn + cn;
+          const double sec = __dadd_rn(__dmul_rn(u, v[2 * lo]), __dmul_rn(t, v[2 * hi]));
+          const double jou = __dadd_rn(__dmul_rn(u, v[2 * lo + 1]), __dmul_rn(t, v[2 * hi + 1]));
+          const double en = __dmul_rn(jou, d.emul);
+          if (k >= K) {
+            p2p_val[k - K] = sec;
+            p2p_val[kMaxClampSlots + k - K] = en;
           }
-          const double first = kn[0], last = kn[n - 1];
-          const bool lo_clamp = x <= first, hi_clamp = x >= last;
-          const int lo = lo_clamp ? 0 : (hi_clamp ? n - 1 : cnt - 1);
-          const int hi = lo_clamp ? 0 : (hi_clamp ? n - 1 : cnt);
-          const double klo = kn[lo], khi = kn[hi];
-          const bool interior = !(lo_clamp || hi_clamp);
-          AxisPos pi;
-          pi.lo = lo;
-          pi.hi = hi;
-          pi.t = __ddiv_rn(interior ? __dsub_rn(x, klo) : 0.0,
-                           interior ? __dsub_rn(khi, klo) : 1.0);
-          pi.clamp = x < first ? -1 : (x > last ? 1 : 0);
-          double t, en;
-          sample(d, tab + d.val_off, pi, t, en);
-          en = __dmul_rn(en, d.emul);
-          const double fl0 = op_flops(d.op, x, d.tasks, d.width, hidden, head_dim);
-          const double by0 = op_bytes(d.op, x, d.tasks, d.width, hidden, kv_elems);
-          const double fl = d.is_cell ? fl0 : 0.0, by = d.is_cell ? by0 : 0.0;
-          const uint32_t bits = (pi.clamp < 0 ? 1u : 0u) | (pi.clamp > 0 ? 2u : 0u) | d.clamp_tw;
-          if (act && bits) atomicOr(&clampbits[di], bits);
-          if (act && di >= C + K) {
-            p2p_val[di - C - K] = t;
-            p2p_val[kMaxClampSlots + di - C - K] = en;
-          }
-          qv[lane] = t;
+          qv[lane] = sec;
           qv[kWarp + lane] = en;
-          qv[2 * kWarp + lane] = fl;
-          qv[3 * kWarp + lane] = by;
+        }
+        if (cell_lane) {
+          qv[lane] = te.x;
+          qv[kWarp + lane] = __dmul_rn(te.y, sdd);  // query_energy * stage_devices
+          qv[2 * kWarp + lane] = fb.x;
+          qv[3 * kWarp + lane] = fb.y;
         }
         __syncwarp();
         const int here = min(kWarp, Q - base);
@@ -637,11 +581,9 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       // block * reps; boundary b adds its p2p to stage b+1
       const double srep = __dmul_rn(bs, reps);
       const double jrep = __dmul_rn(bj, reps);
-      cd = dmax_ref(0.0, srep);
-      ce = __dadd_rn(0.0, jrep);
+      double cd = dmax_ref(0.0, srep);
+      double ce = __dadd_rn(0.0, jrep);
       if (ND <= 2) {
-        // stage b+1 = (block*reps) + p2p of its boundary's (at most two)
-        // distinct tables; max is exact in any order, energies add in order
         const double s0 = __dadd_rn(srep, p2p_val[0]), s1 = __dadd_rn(srep, p2p_val[1]);
         const double j0 = __dadd_rn(jrep, p2p_val[kMaxClampSlots]);
         const double j1 = __dadd_rn(jrep, p2p_val[kMaxClampSlots + 1]);
@@ -655,20 +597,10 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           ce = __dadd_rn(ce, __dadd_rn(jrep, p2p_val[kMaxClampSlots + s]));
         }
       }
-      cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
-      cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
-      if (!mixed && B <= p.memo_cap && lane == 0) {
-        memo[4 * (B - 1) + 1] = ce;
-        memo[4 * (B - 1) + 2] = cf;
-        memo[4 * (B - 1) + 3] = cb;
-        memo[4 * (B - 1)] = cd;
-      }
-      __syncwarp();
+      const double cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
+      const double cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
       PROF_ADD(2, t_ev);
-    }
 
-    bool settle = true;
-    if (mixed) {
       // ---- advance (batching.cpp:78-93) over the prefill frontier ----
       PROF_T0(t_m3);
       clock = __dadd_rn(clock, cd);
@@ -715,6 +647,37 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       PROF_ADD(3, t_m3);
     } else {
       // ---- decode-only run: exact macro-stepping ----
+      PROF_CNT(11);
+      PROF_T0(t_d1);
+      double d, e, f, b;
+      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
+        d = memo[4 * (B - 1)];
+        e = memo[4 * (B - 1) + 1];
+        f = memo[4 * (B - 1) + 2];
+        b = memo[4 * (B - 1) + 3];
+      } else {
+        PROF_CNT(12);
+        const double2* row = reinterpret_cast<const double2*>(dtab + int64_t(B - 1) * 4);
+        const double2 de = __ldg(row), fb = __ldg(row + 1);
+        d = de.x;
+        e = de.y;
+        f = fb.x;
+        b = fb.y;
+        if (B <= p.memo_cap) {
+          if (lane == 0) {
+            memo[4 * (B - 1) + 1] = e;
+            memo[4 * (B - 1) + 2] = f;
+            memo[4 * (B - 1) + 3] = b;
+            memo[4 * (B - 1)] = d;
+          }
+          __syncwarp();
+        }
+      }
+      tok_lo = min(tok_lo, int64_t(B));
+      tok_hi = max(tok_hi, int64_t(B));
+      tot_lo = min(tot_lo, int64_t(B));
+      tot_hi = max(tot_hi, int64_t(B));
+      PROF_ADD(4, t_d1);
       PROF_T0(t_d2);
       // iterations until the first finish (inclusive), cut at the first KV
       // overflow (batching.cpp:112): used + k*B > cap_tok
@@ -732,7 +695,6 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           check = true;  // admissible at iteration start j while used + j*B + ctx fits
         }
       }
-      const double d = cd, e = ce, f = cf, b = cb;
       int64_t j = 0;
       bool stop = false;
       PROF_ADD(5, t_d2);
@@ -875,24 +837,38 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     o.pad = 0;
     p.uout[blockIdx.x] = o;
   }
-  for (int s = lane; s < NQ; s += kWarp) {
-    const uint32_t bits = clampbits[s];
-    const int t = desc[s].table;
-    if (!bits || t < 0) continue;
-    atomicOr((s < C ? p.clamp_compute : p.clamp_curve) + t, bits);
+  // clamp flags from the extreme queried token counts / totals: every
+  // query's x is monotone in its token count (cost.cpp:85-102 locate)
+  if (tok_hi >= 0 && lane < C) {
+    const int g = c0 + lane;
+    const int t = p.cell_tab[size_t(U.fslot) * p.n_cells_total + g];
+    if (t >= 0) {
+      const int nc = p.S.c_n_ctx[t], nt = p.S.c_n_tasks[t], nw = p.S.c_n_width[t];
+      const double* kn = p.S.c_knots + p.S.c_knot_begin[t];
+      const double scale = p.P.cell_scale[g];
+      const double xlo = __dmul_rn(double(tok_lo), scale), xhi = __dmul_rn(double(tok_hi), scale);
+      const AxisPos pj = locate(kn + nc, nt, p.P.cell_tasks[g]);
+      const AxisPos pk = locate(kn + nc + nt, nw, p.P.cell_width[g]);
+      const uint32_t bits = uint32_t(xlo < kn[0]) | uint32_t(xhi > kn[nc - 1]) << 1 |
+                            uint32_t(pj.clamp < 0) << 2 | uint32_t(pj.clamp > 0) << 3 |
+                            uint32_t(pk.clamp < 0) << 4 | uint32_t(pk.clamp > 0) << 5;
+      if (bits) atomicOr(p.clamp_compute + t, bits);
+    }
+  }
+  if (tot_hi >= 0 && lane < NQ) {
+    const CurveDesc& d = cdesc[lane];
+    if (d.table >= 0) {
+      const double xlo = __dmul_rn(__dmul_rn(d.ppt, double(tot_lo)), d.share);
+      const double xhi = __dmul_rn(__dmul_rn(d.ppt, double(tot_hi)), d.share);
+      const double* kn = tab + d.kn_off;
+      const uint32_t bits = uint32_t(xlo < kn[0]) | uint32_t(xhi > kn[d.n - 1]) << 1;
+      if (bits) atomicOr(p.clamp_curve + d.table, bits);
+    }
   }
 }
 
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem) {
   return smem_layout(smem_cap, memo_cap, tab_smem).total;
-}
-
-// Doubles of table staging a unit of this plan needs at most (host side).
-size_t sim_tab_doubles(int n_cells, const int* n_ctx, int n_curves, const int* curve_n) {
-  size_t t = 0;
-  for (int c = 0; c < n_cells; ++c) t += size_t(n_ctx[c]) * (1 + 2 * kMaxCombos);
-  for (int k = 0; k < n_curves; ++k) t += 3 * size_t(curve_n[k]);
-  return t;
 }
 
 }  // namespace psg
