@@ -90,6 +90,7 @@ struct SimParams {
   int32_t anchor;
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
+  int32_t serial_run;        // decode-run iterations stepped serially before the closed form
   int32_t tab_smem;          // doubles of per-unit curve staging in shared memory
   // precomputed cost tables (psg_tables.cu)
   const int32_t* cell_sig;   // [n_freq_slots * n_cells_total] -> cell signature

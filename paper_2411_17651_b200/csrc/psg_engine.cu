@@ -613,6 +613,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.anchor = cfg->ttft_anchor;
   sp.smem_cap = 256;
   sp.memo_cap = 256;
+  sp.serial_run = 128;
+  if (const char* v = std::getenv("PSG_SERIAL_RUN")) sp.serial_run = std::max(1, std::atoi(v));  // dev knob
   sp.tab_smem = tab_smem;
   sp.cell_sig = (const int32_t*)D(o_csig);
   sp.qtab = static_cast<const double*>(ctx->d_qtab.p);

@@ -31,6 +31,7 @@
 #include <climits>
 
 #include "psg_device.cuh"
+#include "psg_fastsum.cuh"
 
 namespace psg {
 
@@ -695,44 +696,81 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           check = true;  // admissible at iteration start j while used + j*B + ctx fits
         }
       }
-      int64_t j = 0;
       bool stop = false;
       PROF_ADD(5, t_d2);
       PROF_T0(t_d3);
-      if (check) {
-        const double a_h = hd_arr;
-        while (j + 4 <= kmax) {
-          const double c1 = __dadd_rn(clock, d);
-          const double c2 = __dadd_rn(c1, d);
-          const double c3 = __dadd_rn(c2, d);
-          if (!(clock < a_h && c1 < a_h && c2 < a_h && c3 < a_h)) break;
-          clock = __dadd_rn(c3, d);
-          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-          j += 4;
-        }
-        while (j < kmax && clock < a_h) {
-          clock = __dadd_rn(clock, d);
-          energy = __dadd_rn(energy, e);
-          flops = __dadd_rn(flops, f);
-          bytes = __dadd_rn(bytes, b);
-          ++j;
-        }
-        if (j < kmax && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) stop = true;
+      // k sequential additions in closed form (psg_fastsum.cuh), bit-exact
+      // Short runs step serially (a dependent DADD per iteration); a run
+      // still going after kSerial iterations finishes in closed form
+      // (psg_fastsum.cuh), bit-exact either way.
+      const int64_t kSerial = p.serial_run;
+      const double a_h = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
+      const int64_t ks = kmax < kSerial ? kmax : kSerial;
+      int64_t j = 0;
+      while (j + 4 <= ks) {
+        const double c1 = __dadd_rn(clock, d);
+        const double c2 = __dadd_rn(c1, d);
+        const double c3 = __dadd_rn(c2, d);
+        if (!(clock < a_h && c1 < a_h && c2 < a_h && c3 < a_h)) break;
+        clock = __dadd_rn(c3, d);
+        energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+        flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+        bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+        j += 4;
       }
-      if (!stop) {
-        for (; j + 4 <= kmax; j += 4) {
-          clock = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(clock, d), d), d), d);
-          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+      while (j < ks && clock < a_h) {
+        clock = __dadd_rn(clock, d);
+        energy = __dadd_rn(energy, e);
+        flops = __dadd_rn(flops, f);
+        bytes = __dadd_rn(bytes, b);
+        ++j;
+      }
+      if (j == ks && j < kmax) {
+        const int64_t j0 = j;
+        if (check) j += fastsum::advance_until(clock, d, kmax - j, a_h);
+        int64_t rest = 0;  // clock additions left after the arrival check
+        if (j < kmax && !(check && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok))) {
+          rest = kmax - j;
+          j = kmax;
         }
-        for (; j < kmax; ++j) {
-          clock = __dadd_rn(clock, d);
-          energy = __dadd_rn(energy, e);
-          flops = __dadd_rn(flops, f);
-          bytes = __dadd_rn(bytes, b);
+        // lanes 0..3 advance clock (rest), energy, flops, bytes (j - j0 each)
+        const double acc = lane == 0 ? clock : lane == 1 ? energy : lane == 2 ? flops : bytes;
+        const double inc = lane == 0 ? d : lane == 1 ? e : lane == 2 ? f : b;
+        const int64_t kk = lane == 0 ? rest : (lane < 4 ? j - j0 : 0);
+        const double r = fastsum::add_n(acc, inc, kk);
+        clock = __shfl_sync(kFull, r, 0);
+        energy = __shfl_sync(kFull, r, 1);
+        flops = __shfl_sync(kFull, r, 2);
+        bytes = __shfl_sync(kFull, r, 3);
+      }
+      if (j < kmax && check && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) {
+        stop = true;
+      } else if (j < kmax) {
+        // the arrived head cannot join this run: finish it (serial part only
+        // reaches here with j < kSerial)
+        const int64_t k2 = kmax - j;
+        if (k2 <= kSerial) {
+          for (; j + 4 <= kmax; j += 4) {
+            clock = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(clock, d), d), d), d);
+            energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+            flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+            bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+          }
+          for (; j < kmax; ++j) {
+            clock = __dadd_rn(clock, d);
+            energy = __dadd_rn(energy, e);
+            flops = __dadd_rn(flops, f);
+            bytes = __dadd_rn(bytes, b);
+          }
+        } else {
+          const double acc = lane == 0 ? clock : lane == 1 ? energy : lane == 2 ? flops : bytes;
+          const double inc = lane == 0 ? d : lane == 1 ? e : lane == 2 ? f : b;
+          const double r = fastsum::add_n(acc, inc, lane < 4 ? k2 : 0);
+          clock = __shfl_sync(kFull, r, 0);
+          energy = __shfl_sync(kFull, r, 1);
+          flops = __shfl_sync(kFull, r, 2);
+          bytes = __shfl_sync(kFull, r, 3);
+          j = kmax;
         }
       }
       PROF_ADD(6, t_d3);

@@ -23,11 +23,17 @@ NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setu
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("key")
+    ap.add_argument("keys", nargs="+")
     ap.add_argument("--top", type=int, default=5)
     ap.add_argument("--workdir", default="/tmp/psg_probe")
     args = ap.parse_args()
     os.environ.setdefault("PSG_LIBRARY", "libpsg_prof.so")
+    for key in args.keys:
+        run(key, args)
+
+
+def run(key, args):
+    args.key = key
     out = os.path.join(args.workdir, f"phase_{args.key}.bin")
     os.makedirs(args.workdir, exist_ok=True)
     os.environ["PSG_PHASE_PROFILE"] = out
@@ -40,7 +46,10 @@ def main():
     meta, cnt = raw[:, :2].view(np.int64), raw[:, 2:]
     order = np.argsort(-cnt[:, 15].astype(np.float64))
     F = max(1, len(case.workload.freqs))
-    print(f"{args.key}: sim {res.ms['sim']:.2f} ms, units {len(raw)}")
+    tots = cnt[:, 15].astype(np.float64)
+    print(f"{args.key}: sim {res.ms['sim']:.2f} ms, units {len(raw)}, "
+          f"sum/max {tots.sum() / tots.max():.1f}, units >50% of max: {(tots > 0.5 * tots.max()).sum()}, "
+          f"totals: {' '.join(f'{k}={cnt[:, k].sum()}' for k in range(10, 14))}")
     for u in order[:args.top]:
         tot = float(cnt[u, 15])
         enc = case.plans.encodings[int(meta[u, 0]) // F]
