@@ -92,6 +92,7 @@ struct SimParams {
   int32_t memo_cap;          // decode-cost memo entries in shared memory
   int32_t serial_run;        // decode-run iterations stepped serially before the closed form
   int32_t tab_smem;          // doubles of per-unit curve staging in shared memory
+  int32_t cm2_cap;           // finish-summary groups (1024 slots each) in shared memory
   // precomputed cost tables (psg_tables.cu)
   const int32_t* cell_sig;   // [n_freq_slots * n_cells_total] -> cell signature
   const double* qtab;        // per signature, per token count: {t, e_raw, flops, bytes}
@@ -111,6 +112,7 @@ struct SimParams {
   unsigned long long* prof;  // PSG_PHASE_PROFILE builds: kProfSlots counters per unit
   int32_t* g_i32;            // kGI32 int32 arrays per unit, stride n_req
   double* g_f64;             // kGF64 8-byte arrays per unit, stride n_req
+  int64_t* g_cm;             // per-unit chunk minima once the active slots live in global memory
 };
 
 // Parameters of the cost-table kernels (psg_tables.cu).

@@ -122,10 +122,12 @@ const char* dtype_name(int d) {
 
 struct psg_context {
   int device = 0;
+  int n_sm = 148;                  // device properties used to size the simulation launch
+  int64_t smem_sm = 228 * 1024, smem_block_max = 227 * 1024;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
-  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
+  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
@@ -161,6 +163,14 @@ int psg_context_create(int device, psg_context** out) {
   if (cudaSetDevice(device) != cudaSuccess) return PSG_ERR_CUDA;
   auto* ctx = new psg_context();
   ctx->device = device;
+  {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) ctx->n_sm = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device) == cudaSuccess && v > 0)
+      ctx->smem_sm = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)
+      ctx->smem_block_max = v;
+  }
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return PSG_ERR_CUDA;
@@ -175,7 +185,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
-                    &ctx->d_scratch_f64, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof})
+                    &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj}) b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
@@ -562,6 +572,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(ctx->d_slot_u8.ensure(std::max<size_t>(slots, 1)));
   PSG_CUDA(ctx->d_scratch_i32.ensure(std::max<int64_t>(scratch_total, 1) * kScratchI32 * sizeof(int32_t)));
   PSG_CUDA(ctx->d_scratch_f64.ensure(std::max<int64_t>(scratch_total, 1) * kScratchF64 * sizeof(double)));
+  // chunk minima once a unit's slots migrate: unit k uses [S_k/32 + 2k, +n_req/32 + 2)
+  PSG_CUDA(ctx->d_scratch_cm.ensure((scratch_total / 32 + 2 * int64_t(n_units) + 2) * sizeof(int64_t)));
   PSG_CUDA(ctx->d_qtab.ensure(size_t(std::max<int64_t>(qrows, 1)) * 4 * sizeof(double)));
   PSG_CUDA(ctx->d_dtab.ensure(size_t(std::max<int64_t>(drows, 1)) * 4 * sizeof(double)));
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
@@ -611,11 +623,34 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.chunk_size = cfg->chunk_size;
   sp.max_batch_size = cfg->max_batch_size;
   sp.anchor = cfg->ttft_anchor;
-  sp.smem_cap = 256;
   sp.memo_cap = 256;
+  sp.tab_smem = tab_smem;
+  {
+    // Active slots live in shared memory while they fit: give each unit as
+    // many as keeps every unit resident in one wave (the kernel's time is its
+    // longest unit), at least 256, at most the largest unit's request count.
+    int64_t max_nr = 0;
+    for (const auto& u : units) max_nr = std::max<int64_t>(max_nr, u.n_req);
+    const int64_t want = std::max<int64_t>(256, (max_nr + 31) / 32 * 32);
+    const int per_sm = std::max(1, (n_units + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
+    const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024);
+    int64_t cap = 256;
+    for (int64_t c = want; c > 256; c -= 32) {
+      const int64_t l2 = (std::max<int64_t>(c, max_nr) + 1023) / 1024 + 1;
+      if (int64_t(sim_smem_bytes(int(c), sp.memo_cap, tab_smem, int(l2))) <= budget) {
+        cap = c;
+        break;
+      }
+    }
+    sp.smem_cap = int(cap);
+  }
   sp.serial_run = 128;
   if (const char* v = std::getenv("PSG_SERIAL_RUN")) sp.serial_run = std::max(1, std::atoi(v));  // dev knob
-  sp.tab_smem = tab_smem;
+  {
+    int64_t max_len = sp.smem_cap;  // active slots never exceed max(smem_cap, n_req)
+    for (const auto& u : units) max_len = std::max<int64_t>(max_len, u.n_req);
+    sp.cm2_cap = int((max_len + 1023) / 1024 + 1);
+  }
   sp.cell_sig = (const int32_t*)D(o_csig);
   sp.qtab = static_cast<const double*>(ctx->d_qtab.p);
   sp.qoff = (const int64_t*)D(o_qoff);
@@ -666,6 +701,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   }
   sp.g_i32 = static_cast<int32_t*>(ctx->d_scratch_i32.p);
   sp.g_f64 = static_cast<double*>(ctx->d_scratch_f64.p);
+  sp.g_cm = static_cast<int64_t*>(ctx->d_scratch_cm.p);
 
   ReduceParams rp{};
   rp.n_slots = N;
@@ -696,7 +732,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaMemsetAsync(sp.slot_status, 0, std::max<size_t>(slots, 1), st));
   PSG_CUDA(cudaMemsetAsync(W(w_cc), 0, wk.size - w_cc, st));
   PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
-  const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem);
+  const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem, sp.cm2_cap);
+  if (prof_path) std::fprintf(stderr, "psg: units=%d smem_cap=%d smem=%zu B\n", n_units, sp.smem_cap, smem);
   PSG_CUDA(cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (n_sig > 0) {  // cell-query tables, then decode-only iteration tables
     qtab_kernel<<<dim3(unsigned(n_sig), unsigned((max_qrows + 255) / 256)), 256, 0, st>>>(tp);

@@ -84,9 +84,15 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
   const size_t base = size_t(e) * size_t(r.n_slots);
   const uint8_t* st = r.slot_status + base;
   const double* ttft = r.slot_ttft + base;
-  const double* tpot = r.slot_tpot + base;
+  double* tpot = r.slot_tpot + base;
   const double* e2e = r.slot_e2e + base;
   const int64_t* gen = r.slot_gen;  // per slot (id order), shared by entries
+
+  // The simulation stores tpot's numerator (finish clock - first token);
+  // the division (simulator.cpp:150-152) runs here, off its serial path.
+  for (int64_t i = threadIdx.x; i < r.n_slots; i += blockDim.x)
+    if (st[i] == 1) tpot[i] = gen[i] >= 2 ? __ddiv_rn(tpot[i], double(gen[i] - 1)) : 0.0;
+  __syncthreads();
 
   // ---- ordered means: one serial chain in ascending id order (warp 0) ----
   if (threadIdx.x < 32) {

@@ -19,7 +19,8 @@ struct EntryOut {
 struct ReduceParams {
   int64_t n_slots;
   const uint8_t* slot_status;
-  const double *slot_ttft, *slot_tpot, *slot_e2e;
+  const double *slot_ttft, *slot_e2e;
+  double* slot_tpot;  // numerators from the simulation; divided in place by entry_reduce_kernel
   const int64_t* slot_gen;   // gen_len by slot (id order)
   const int64_t* slot_id;    // id by slot
   const UnitOut* uout;
@@ -46,7 +47,7 @@ __global__ void compact_kernel(const ReduceParams r, const int64_t* pr_off,
                                int64_t* out_rj);
 __global__ void rank_kernel(const psg_rank_key* keys, int64_t n, int64_t* order);
 
-size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem);
+size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap);
 __global__ void qtab_kernel(const TabParams p);
 __global__ void dectab_kernel(const TabParams p);
 constexpr int kScratchI32 = 7, kScratchF64 = 4;  // per-unit global fallback arrays

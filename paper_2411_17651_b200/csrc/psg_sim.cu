@@ -40,6 +40,7 @@ namespace {
 constexpr int64_t kNoFin = INT64_MAX;  // prefill phase
 constexpr int64_t kDead = INT64_MIN;   // tombstone (finished / evicted slot)
 constexpr unsigned kNoRel = 0xffffffffu;
+constexpr int kQvStride = kWarp + 1;  // query-value rows; +1 keeps lanes 0..3 on distinct banks
 constexpr int kGI32 = 7;  // global fallback arrays: stack, tidx, ctx, gen, done, slot, items
 constexpr int kGF64 = 4;  // adm, ft, arr, fin
 
@@ -69,7 +70,7 @@ struct ActiveList {
 
 // A collective / p2p curve staged in shared memory (cost.cpp:262-291).
 struct CurveDesc {
-  int kn_off, n, table, pad;
+  int kn_off, n, table, hint;  // hint: last interior interval (knot index) queried
   double ppt, share, emul;  // payload = (ppt * tokens) * share; energy * emul
 };
 
@@ -77,13 +78,13 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 
 struct SmemLayout {
   size_t qv, cdesc, cellq, p2p_slot, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
-      tab, total;
+      cm1, cm2, tab, total;
 };
 
-__host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem) {
+__host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {
   SmemLayout L;
   size_t o = 0;
-  L.qv = o;        o = al16(o + sizeof(double) * 4 * kWarp);
+  L.qv = o;        o = al16(o + sizeof(double) * 4 * kQvStride);
   L.cdesc = o;     o = al16(o + sizeof(CurveDesc) * kMaxClampSlots);
   L.cellq = o;     o = al16(o + sizeof(int64_t) * kMaxCells);
   L.p2p_slot = o;  o = al16(o + kMaxClampSlots);
@@ -94,6 +95,8 @@ __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_s
   L.act_f64 = o;   o = al16(o + sizeof(double) * 3 * size_t(smem_cap));
   L.act_fin = o;   o = al16(o + sizeof(int64_t) * size_t(smem_cap));
   L.act_i32 = o;   o = al16(o + sizeof(int32_t) * 6 * size_t(smem_cap));
+  L.cm1 = o;       o = al16(o + sizeof(int64_t) * size_t(smem_cap / kWarp + 1));
+  L.cm2 = o;       o = al16(o + sizeof(int64_t) * size_t(cm2_cap));
   L.tab = o;       o = al16(o + sizeof(double) * size_t(tab_smem));
   L.total = o;
   return L;
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
 #endif
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem);
+  const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap);
   double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
   CurveDesc* cdesc = reinterpret_cast<CurveDesc*>(smem_raw + L.cdesc);
   int64_t* cellq = reinterpret_cast<int64_t*>(smem_raw + L.cellq);  // qtab row 0 of each cell
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       d.emul = 1.0;
     }
     d.n = d.table >= 0 ? p.S.k_n[d.table] : 1;
-    d.pad = 0;
+    d.hint = 0;
     cdesc[lane] = d;
   }
   __syncwarp();
@@ -235,6 +238,12 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   int32_t* g_i = p.g_i32 + size_t(U.scratch) * kGI32;  // [stack | tidx ctx gen done slot items]
   double* g_f = p.g_f64 + size_t(U.scratch) * kGF64;   // [adm | ft | arr | fin]
   int32_t* g_stack = g_i;
+  // Finish summary: cm1[c] = min decode fin of slots [32c, 32c+32), cm2[g] =
+  // min of cm1 over chunks [32g, 32g+32) (kNoFin if none).  A finish event
+  // visits only the groups / chunks whose minimum is due.
+  int64_t* cm1 = reinterpret_cast<int64_t*>(smem_raw + L.cm1);
+  int64_t* cm2 = reinterpret_cast<int64_t*>(smem_raw + L.cm2);
+  int64_t* g_cm = p.g_cm + (U.scratch >> 5) + 2 * int64_t(blockIdx.x);
 
   auto req_tidx = [&](int j) -> int {
     return p.T.seq ? p.T.seq[U.seq_base + j]
@@ -257,7 +266,9 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   int64_t next_fin = kNoFin;
   int err = 0;
   // extreme cell-query token counts and iteration totals (clamp reporting)
-  int64_t tok_lo = INT64_MAX, tok_hi = -1, tot_lo = INT64_MAX, tot_hi = -1;
+  int tok_lo = INT_MAX, tok_hi = -1;          // cell token counts (< 2^31)
+  int64_t tot_lo = INT64_MAX, tot_hi = -1;     // iteration totals
+  int run_lo = INT_MAX, run_hi = -1;           // decode-run batch sizes (both of the above)
 
   // pending head (batching.hpp:93 pending_.front()), warp-uniform registers
   bool hd_valid = false, hd_stack = false;
@@ -310,6 +321,32 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   auto min_rel = [&](int64_t fin, int64_t base) -> unsigned {  // decode slots only
     return (fin == kNoFin || fin == kDead) ? kNoRel : unsigned(fin - base);
   };
+  auto rel_of = [&](int64_t v) -> unsigned {  // v: kNoFin or a fin >= n
+    return v == kNoFin ? kNoRel : unsigned(v - n);
+  };
+  auto abs_of = [&](unsigned r) -> int64_t { return r == kNoRel ? kNoFin : n + int64_t(r); };
+  // cm2[g] from the chunk minima of group g
+  auto fix_group = [&](int g) {
+    __syncwarp();
+    const int nch = (len + kWarp - 1) / kWarp;
+    const int c = g * kWarp + lane;
+    const unsigned r = __reduce_min_sync(kFull, c < nch ? rel_of(cm1[c]) : kNoRel);
+    if (lane == 0) cm2[g] = abs_of(r);
+    __syncwarp();
+  };
+  // cm1[c] from the slots of chunk c
+  auto fix_chunk = [&](int c) {
+    __syncwarp();
+    const int i = c * kWarp + lane;
+    const unsigned r = __reduce_min_sync(kFull, i < len ? min_rel(a.fin[i], n) : kNoRel);
+    if (lane == 0) cm1[c] = abs_of(r);
+    __syncwarp();
+  };
+  auto rebuild_summary = [&]() {
+    const int nch = (len + kWarp - 1) / kWarp;
+    for (int c = 0; c < nch; ++c) fix_chunk(c);
+    for (int g = 0; g * kWarp < nch; ++g) fix_group(g);
+  };
   // Order-preserving in-place compaction of the live slots.
   auto compact = [&]() {
     __syncwarp();
@@ -350,6 +387,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     }
     len = w;
     first_pre = below;
+    rebuild_summary();
   };
   auto migrate = [&]() {
     // Move the active slots to the unit's global region: capacity n_req.
@@ -379,6 +417,9 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     a.ft = g_f + nr;
     a.arr = g_f + 2 * nr;
     a.fin = gfin;
+    for (int c = lane; c <= p.smem_cap / kWarp; c += kWarp) g_cm[c] = cm1[c];
+    __syncwarp();
+    cm1 = g_cm;
     cap_now = int(nr);
   };
   // Drops trailing tombstones so slot len-1 is the newest live request.
@@ -397,12 +438,13 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     first_pre = first_pre < len ? first_pre : len;
   };
   auto recompute_next_fin = [&]() {
+    const int ng = ((len + kWarp - 1) / kWarp + kWarp - 1) / kWarp;
     unsigned m = kNoRel;
-    for (int base = 0; base < len; base += kWarp) {
-      const int i = base + lane;
-      m = min(m, __reduce_min_sync(kFull, i < len ? min_rel(a.fin[i], n) : kNoRel));
+    for (int base = 0; base < ng; base += kWarp) {
+      const int g = base + lane;
+      m = min(m, __reduce_min_sync(kFull, g < ng ? rel_of(cm2[g]) : kNoRel));
     }
-    next_fin = m == kNoRel ? kNoFin : n + m;
+    next_fin = abs_of(m);
   };
 
   load_head();
@@ -418,6 +460,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           if (len >= cap_now) migrate();
         }
         if (lane == 0) {
+          if ((len & (kWarp - 1)) == 0) cm1[len / kWarp] = kNoFin;  // fresh chunk / group
+          if ((len & (kWarp * kWarp - 1)) == 0) cm2[len / (kWarp * kWarp)] = kNoFin;
           a.tidx[len] = hd_tidx;
           a.ctx[len] = hd_ctx;
           a.gen[len] = hd_gen;
@@ -478,11 +522,13 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       __syncwarp();
       const int64_t decode = int64_t(B) - n_items;
       const int64_t total = decode + pre_tok;
-      tok_lo = min(tok_lo, int64_t(it_lo));
-      tok_hi = max(tok_hi, int64_t(it_hi));
+      if (n_items > 0) {
+        tok_lo = min(tok_lo, int(it_lo));
+        tok_hi = max(tok_hi, int(it_hi));
+      }
       if (decode > 0) {
-        tok_lo = min(tok_lo, decode);
-        tok_hi = max(tok_hi, decode);
+        tok_lo = min(tok_lo, int(decode));
+        tok_hi = max(tok_hi, int(decode));
       }
       tot_lo = min(tot_lo, total);
       tot_hi = max(tot_hi, total);
@@ -494,7 +540,11 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       const int Qc = C * nq_c;
       const int Q = Qc + NQ;
       const double total_d = double(total);
-      double bs = 0.0, bj = 0.0, bf = 0.0, bb = 0.0;
+      // lanes 0..3 run the four reference-ordered chains (seconds, joules,
+      // flops, bytes); lanes 2, 3 stop at the cells (collectives add none)
+      double chain = 0.0;
+      const double* qrow = qv + (lane < 4 ? lane : 0) * kQvStride;
+      const float inv_nq = __frcp_rn(float(nq_c));
       for (int base = 0; base < Q; base += kWarp) {
         const int q = base + lane;
         // cell query = one precomputed row {t, e_raw, flops, bytes}: issue the
@@ -502,7 +552,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
         const bool cell_lane = q < Qc;
         double2 te = make_double2(0.0, 0.0), fb = make_double2(0.0, 0.0);
         if (cell_lane) {
-          const int c = q / nq_c;
+          const int c = int((float(q) + 0.5f) * inv_nq);  // q / nq_c (q, nq_c < 2^16)
           const int i = q - c * nq_c;
           const int64_t tok = i < n_items ? int64_t(a.items[i]) : decode;
           const double2* row = reinterpret_cast<const double2*>(qtab + (cellq[c] + tok) * 4);
@@ -512,13 +562,21 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
         if (!cell_lane && q < Q) {
           // collective / p2p curve query on the staged curve
           const int k = q - Qc;
-          const CurveDesc& d = cdesc[k];
+          CurveDesc& d = cdesc[k];
           const double x = __dmul_rn(__dmul_rn(d.ppt, total_d), d.share);
           const double* kn = tab + d.kn_off;
           const int cn = d.n;
-          int cnt = 0;
-          for (int j = 0; j < n_curve_knots; ++j)
-            cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
+          // cnt = #knots <= x; the last interval usually still holds
+          const int h = d.hint;
+          int cnt;
+          if (h + 1 < cn && kn[h] <= x && x < kn[h + 1]) {
+            cnt = h + 1;
+          } else {
+            cnt = 0;
+            for (int j = 0; j < n_curve_knots; ++j)
+              cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
+            if (cnt >= 1 && cnt < cn) d.hint = cnt - 1;
+          }
           const bool lo_c = x <= kn[0], hi_c = x >= kn[cn - 1];
           const int lo = lo_c ? 0 : (hi_c ? cn - 1 : cnt - 1);
           const int hi = lo_c ? 0 : (hi_c ? cn - 1 : cnt);
@@ -535,49 +593,32 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
             p2p_val[kMaxClampSlots + k - K] = en;
           }
           qv[lane] = sec;
-          qv[kWarp + lane] = en;
+          qv[kQvStride + lane] = en;
         }
         if (cell_lane) {
           qv[lane] = te.x;
-          qv[kWarp + lane] = __dmul_rn(te.y, sdd);  // query_energy * stage_devices
-          qv[2 * kWarp + lane] = fb.x;
-          qv[3 * kWarp + lane] = fb.y;
+          qv[kQvStride + lane] = __dmul_rn(te.y, sdd);  // query_energy * stage_devices
+          qv[2 * kQvStride + lane] = fb.x;
+          qv[3 * kQvStride + lane] = fb.y;
         }
         __syncwarp();
+        PROF_ADD(14, t_ev);
         const int here = min(kWarp, Q - base);
         const int cell_end = min(here, max(0, Qc - base));
         const int coll_end = min(here, max(0, Qc + K - base));
-        // loads first (independent), then the reference-ordered FP64 chains
+        const int end = lane < 2 ? coll_end : (lane < 4 ? cell_end : 0);
         int l = 0;
-        for (; l + 4 <= cell_end; l += 4) {
-          double t[4], e[4], f[4], y[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            t[u] = qv[l + u];
-            e[u] = qv[kWarp + l + u];
-            f[u] = qv[2 * kWarp + l + u];
-            y[u] = qv[3 * kWarp + l + u];
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            bs = __dadd_rn(bs, t[u]);
-            bj = __dadd_rn(bj, e[u]);
-            bf = __dadd_rn(bf, f[u]);
-            bb = __dadd_rn(bb, y[u]);
-          }
+        for (; l + 4 <= end; l += 4) {
+          const double v0 = qrow[l], v1 = qrow[l + 1], v2 = qrow[l + 2], v3 = qrow[l + 3];
+          chain = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(chain, v0), v1), v2), v3);
         }
-        for (; l < cell_end; ++l) {
-          bs = __dadd_rn(bs, qv[l]);
-          bj = __dadd_rn(bj, qv[kWarp + l]);
-          bf = __dadd_rn(bf, qv[2 * kWarp + l]);
-          bb = __dadd_rn(bb, qv[3 * kWarp + l]);
-        }
-        for (; l < coll_end; ++l) {
-          bs = __dadd_rn(bs, qv[l]);
-          bj = __dadd_rn(bj, qv[kWarp + l]);
-        }
+        for (; l < end; ++l) chain = __dadd_rn(chain, qrow[l]);
         __syncwarp();
       }
+      const double bs = __shfl_sync(kFull, chain, 0);
+      const double bj = __shfl_sync(kFull, chain, 1);
+      const double bf = __shfl_sync(kFull, chain, 2);
+      const double bb = __shfl_sync(kFull, chain, 3);
       // stages (simulator.cpp:64-78, :125-130): every stage prices the same
       // block * reps; boundary b adds its p2p to stage b+1
       const double srep = __dmul_rn(bs, reps);
@@ -613,7 +654,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       const int64_t n_new = n + 1;
       unsigned ncompl = 0, m = min_rel(next_fin, n_new);
       int new_fp = -1;
-      for (int base = first_pre; base < len; base += kWarp) {
+      for (int base = first_pre & ~(kWarp - 1); base < len; base += kWarp) {  // whole chunks
         const int i = base + lane;
         bool compl_now = false, still = false;
         unsigned rel = kNoRel;
@@ -635,7 +676,14 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           }
         }
         ncompl += __popc(__ballot_sync(kFull, compl_now));
-        m = min(m, __reduce_min_sync(kFull, rel));
+        const unsigned cr = __reduce_min_sync(kFull, rel);
+        m = min(m, cr);
+        if (cr != kNoRel && lane == 0) {  // new decode slots in this chunk
+          const int64_t v = n_new + int64_t(cr);
+          const int c = base / kWarp;
+          cm1[c] = min(cm1[c], v);
+          cm2[c / kWarp] = min(cm2[c / kWarp], v);
+        }
         const unsigned sm = __ballot_sync(kFull, still);
         if (new_fp < 0 && sm) new_fp = base + __ffs(sm) - 1;
       }
@@ -674,10 +722,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
           __syncwarp();
         }
       }
-      tok_lo = min(tok_lo, int64_t(B));
-      tok_hi = max(tok_hi, int64_t(B));
-      tot_lo = min(tot_lo, int64_t(B));
-      tot_hi = max(tot_hi, int64_t(B));
+      run_lo = min(run_lo, B);
+      run_hi = max(run_hi, B);
       PROF_ADD(4, t_d1);
       PROF_T0(t_d2);
       // iterations until the first finish (inclusive), cut at the first KV
@@ -790,31 +836,54 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       PROF_CNT(13);
       int64_t freed = 0;
       unsigned m = kNoRel, nfin = 0;
-      for (int base = 0; base < len; base += kWarp) {
-        const int i = base + lane;
-        const int64_t fin = i < len ? a.fin[i] : kDead;
-        const bool fnow = fin == n;
-        unsigned tok = 0;
-        if (fnow) {
-          const int32_t gen = a.gen[i];
-          const double arr = a.arr[i], ft = a.ft[i];
-          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
-          const size_t s = slot_base + a.slot[i];
-          p.slot_e2e[s] = __dsub_rn(clock, arr);
-          p.slot_ttft[s] = __dsub_rn(ft, anchor);
-          p.slot_tpot[s] = gen >= 2 ? __ddiv_rn(__dsub_rn(clock, ft), double(gen - 1)) : 0.0;
-          p.slot_status[s] = 1;
-          a.fin[i] = kDead;
-          tok = unsigned(a.ctx[i] + gen);
+      const int nch = (len + kWarp - 1) / kWarp;
+      const int ng = (nch + kWarp - 1) / kWarp;
+      for (int gb = 0; gb < ng; gb += kWarp) {
+        const int g = gb + lane;
+        const int64_t v2 = g < ng ? cm2[g] : kNoFin;
+        unsigned gm = __ballot_sync(kFull, v2 == n);
+        m = min(m, __reduce_min_sync(kFull, v2 == n ? kNoRel : rel_of(v2)));
+        while (gm) {
+          const int grp = gb + __ffs(gm) - 1;
+          gm &= gm - 1;
+          const int c = grp * kWarp + lane;
+          int64_t v1 = c < nch ? cm1[c] : kNoFin;
+          unsigned cmask = __ballot_sync(kFull, v1 == n);
+          while (cmask) {
+            const int cl = __ffs(cmask) - 1;
+            cmask &= cmask - 1;
+            const int i = (grp * kWarp + cl) * kWarp + lane;
+            const int64_t fin = i < len ? a.fin[i] : kDead;
+            const bool fnow = fin == n;
+            unsigned tok = 0;
+            if (fnow) {
+              const int32_t gen = a.gen[i];
+              const double arr = a.arr[i], ft = a.ft[i];
+              const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
+              const size_t s = slot_base + a.slot[i];
+              p.slot_e2e[s] = __dsub_rn(clock, arr);
+              p.slot_ttft[s] = __dsub_rn(ft, anchor);
+              p.slot_tpot[s] = __dsub_rn(clock, ft);  // / (gen - 1) in entry_reduce_kernel
+              p.slot_status[s] = 1;
+              a.fin[i] = kDead;
+              tok = unsigned(a.ctx[i] + gen);
+            }
+            freed += int64_t(__reduce_add_sync(kFull, tok));
+            nfin += __popc(__ballot_sync(kFull, fnow));
+            const unsigned cr = __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n));
+            if (lane == cl) v1 = abs_of(cr);
+            if (lane == 0) cm1[grp * kWarp + cl] = abs_of(cr);
+          }
+          const unsigned gr = __reduce_min_sync(kFull, rel_of(v1));
+          if (lane == 0) cm2[grp] = abs_of(gr);
+          m = min(m, gr);
         }
-        freed += int64_t(__reduce_add_sync(kFull, tok));
-        nfin += __popc(__ballot_sync(kFull, fnow));
-        m = min(m, __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n)));
       }
+      __syncwarp();
       B -= int(nfin);
       completed += nfin;
       used -= freed;
-      next_fin = m == kNoRel ? kNoFin : n + m;
+      next_fin = abs_of(m);
       trim();
       if (len > 2 * B + 2 * kWarp) compact();
     }
@@ -836,6 +905,10 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       --B;
       evicted = true;
       trim();
+      if (fin != kNoFin) {  // a decode slot left the summary
+        fix_chunk(i / kWarp);
+        fix_group(i / (kWarp * kWarp));
+      }
     }
     if (B == 1 && used > cap_tok) {  // a lone outgrowing request is rejected
       reject_slot(a.slot[len - 1]);
@@ -877,6 +950,12 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   }
   // clamp flags from the extreme queried token counts / totals: every
   // query's x is monotone in its token count (cost.cpp:85-102 locate)
+  if (run_hi >= 0) {
+    tok_lo = min(tok_lo, run_lo);
+    tok_hi = max(tok_hi, run_hi);
+    tot_lo = min(tot_lo, int64_t(run_lo));
+    tot_hi = max(tot_hi, int64_t(run_hi));
+  }
   if (tok_hi >= 0 && lane < C) {
     const int g = c0 + lane;
     const int t = p.cell_tab[size_t(U.fslot) * p.n_cells_total + g];
@@ -905,8 +984,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   }
 }
 
-size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem) {
-  return smem_layout(smem_cap, memo_cap, tab_smem).total;
+size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {
+  return smem_layout(smem_cap, memo_cap, tab_smem, cm2_cap).total;
 }
 
 }  // namespace psg
