@@ -282,6 +282,14 @@ struct SimConfig {
   double freq_ghz = 0.0;
   BatchPolicy policy;
   TtftAnchor ttft_anchor = TtftAnchor::Arrival;
+  bool emit_iterations = false;  // simulate_plan only (simulator.hpp:77)
+};
+
+// plansim::IterationRecord (simulator.hpp:35-42).
+struct IterationRecord {
+  double clock_start = 0.0, duration = 0.0, energy = 0.0;
+  int64_t batch_size = 0;
+  std::vector<double> stage_seconds, stage_joules;
 };
 enum class Objective { Latency, Energy };
 
@@ -301,6 +309,17 @@ struct SimulationReport {
   double p50_ttft = 0.0, p99_ttft = 0.0, p50_tpot = 0.0, p99_tpot = 0.0;
   std::vector<RequestMetrics> per_request;
   std::vector<int64_t> rejected_ids;
+  std::vector<IterationRecord> iterations;  // emit_iterations
+};
+
+// plansim::SweepRow / SweepTable (simulator.hpp:105-115).
+struct SweepRow {
+  int64_t max_batch_size = 0;
+  double mean_tpot = 0.0, mean_ttft = 0.0, e2e_latency = 0.0;
+};
+struct SweepTable {
+  int64_t observed_max_batch = 0;
+  std::vector<SweepRow> rows;
 };
 
 struct SearchEntry {
@@ -347,10 +366,17 @@ RankedPlans search(const std::vector<ExecutionPlan>& plans, const ModelSpec& mod
                    Objective objective, const std::vector<double>& frequencies,
                    const SimConfig& cfg, int jobs = 1, Engine* engine = nullptr);
 
-// plansim::simulate_plan (simulator.hpp:80-82).
+// plansim::simulate_plan (simulator.hpp:80-82), emit_iterations included.
 SimulationReport simulate_plan(const ExecutionPlan& plan, const ModelSpec& model,
                                const ClusterSpec& cluster, const Trace& trace,
                                const ProfileStore& store, const SimConfig& cfg,
                                Engine* engine = nullptr);
+
+// plansim::sweep_max_batch (simulator.hpp:117-122): the capped simulations
+// run in one launch.
+SweepTable sweep_max_batch(const ExecutionPlan& plan, const ModelSpec& model,
+                           const ClusterSpec& cluster, const Trace& trace,
+                           const ProfileStore& store, const SimConfig& cfg, int segments,
+                           int64_t subset_size = 256, Engine* engine = nullptr);
 
 }  // namespace psb

@@ -168,7 +168,25 @@ typedef struct psg_config {
   int32_t rank;                       /* 1: sort entries (search); 0: entry order */
   int32_t n_entry_subset;             /* >0: simulate only these entry indices (sharding) */
   const int32_t* entry_subset;
+  /* per-entry override of max_batch_size (one value per simulated entry:
+     per entry_subset element, else per global entry; NULL = none).  With a
+     repeated entry_subset this runs several BatchPolicy caps of one plan in
+     one launch (sweep_max_batch, simulator.cpp:298-329). */
+  const int64_t* entry_max_batch_size;
+  /* SimConfig::emit_iterations (simulator.hpp:77): one IterationRecord per
+     iteration (simulator.cpp:158-170); requires exactly one entry */
+  int32_t emit_iterations;
 } psg_config;
+
+/* plansim::IterationRecord (simulator.hpp:35-42) without the stage vectors,
+   which are returned as psg_result.stage_seconds / stage_joules with stride
+   psg_result.n_stages. */
+typedef struct psg_iteration {
+  double clock_start;
+  double duration;                    /* max over stages */
+  double energy;                      /* sum over stages */
+  int64_t batch_size;
+} psg_iteration;
 
 /* plansim::RequestMetrics (simulator.hpp:44-50); identical layout (40 B). */
 typedef struct psg_request_metrics {
@@ -237,6 +255,13 @@ typedef struct psg_result {
   int64_t sum_batch;                  /* sum over all iterations of the batch size */
   int64_t admissions;                 /* admissions, re-admissions included */
   int64_t finishes;                   /* completed requests */
+  /* emit_iterations: records of all replicas in replica order (run_replica
+     appends replica by replica, simulator.cpp:196-199) */
+  int64_t n_iterations;
+  psg_iteration* iterations;
+  int32_t n_stages;
+  double* stage_seconds;              /* [n_iterations][n_stages] */
+  double* stage_joules;               /* [n_iterations][n_stages] */
 } psg_result;
 
 typedef struct psg_context psg_context;

@@ -14,6 +14,8 @@
 //                   [--out-result F] [--out-plans F] [--out-store F] [--out-trace F]
 //   refdrv simulate <inputs> [sim flags] --plan-spec dp,pp,mode:cdp:intra,...
 //                   [--out-result F] [--emit-iterations F]
+//   refdrv sweep    <inputs> [sim flags] --plan-spec ... --segments N [--subset M]
+//                   (prints the SweepTable with hex floats)
 //   refdrv synth    --model F --cluster F [--synth-profiles MAXCTX] [--synth-trace ...]
 //                   [--out-store F] [--out-trace F]
 // inputs:  --model F --cluster F (--profiles F | --synth-profiles MAXCTX)
@@ -64,6 +66,8 @@ struct Args {
   long long plan_lo = 0, plan_hi = -1;
   std::string plan_spec;
   std::string out_result, out_plans, out_store, out_trace, emit_iterations;
+  int segments = 4;
+  long long subset = 256;
 };
 
 std::vector<double> split_doubles(const std::string& s) {
@@ -112,6 +116,8 @@ Args parse(int argc, char** argv) {
     else if (k == "--out-store") a.out_store = v();
     else if (k == "--out-trace") a.out_trace = v();
     else if (k == "--emit-iterations") a.emit_iterations = v();
+    else if (k == "--segments") a.segments = std::stoi(v());
+    else if (k == "--subset") a.subset = std::stoll(v());
     else throw DataError("unknown flag " + k);
   }
   return a;
@@ -311,6 +317,23 @@ int run(const Args& a) {
     if (!a.out_plans.empty()) write_file(a.out_plans, plans_json({plan}));
     std::printf("{\"cmd\":\"simulate\",\"iterations\":%lld,\"seconds\":%.9g}\n",
                 (long long)r.num_iterations, dt);
+    return 0;
+  }
+
+  if (a.cmd == "sweep") {
+    const ExecutionPlan plan = plan_from_spec(a.plan_spec, model, block, cluster, popt);
+    SimConfig run_cfg = cfg;
+    if (!a.freqs.empty()) run_cfg.freq_ghz = a.freqs.front();
+    const SweepTable t =
+        sweep_max_batch(plan, model, cluster, trace, store, run_cfg, a.segments, a.subset);
+    if (!a.out_plans.empty()) write_file(a.out_plans, plans_json({plan}));
+    std::printf("{\"cmd\":\"sweep\",\"observed_max_batch\":%lld,\"rows\":[",
+                (long long)t.observed_max_batch);
+    for (size_t i = 0; i < t.rows.size(); ++i)
+      std::printf("%s[%lld,\"%a\",\"%a\",\"%a\"]", i ? "," : "",
+                  (long long)t.rows[i].max_batch_size, t.rows[i].mean_tpot, t.rows[i].mean_ttft,
+                  t.rows[i].e2e_latency);
+    std::printf("]}\n");
     return 0;
   }
 

@@ -9,6 +9,10 @@
 //        (--trace F | --synth-trace a,b,c,d,rate,n,seed) [--objective energy]
 //        [--freqs a,b] [--batching chunked --chunk N] [--max-batch N]
 //        [--anchor admission] [--jobs N] [--drop-table OP]
+//        [--single K [--sweep-segments S --sweep-subset M]]
+// --single K additionally compares simulate_plan(plans[K]) with
+// emit_iterations (every IterationRecord) and, with --sweep-segments,
+// sweep_max_batch (every SweepRow).
 // Prints one JSON line; exit 0 on full parity, 1 on a mismatch, 3/4 when both
 // implementations raise the same InfeasibleError / DataError.
 #include <chrono>
@@ -50,7 +54,8 @@ int main(int argc, char** argv) {
   double synth_ctx = 0;
   std::vector<double> synth_tr, freqs;
   SimConfig cfg;
-  int jobs = 1;
+  int jobs = 1, single = -1, sweep_segments = 0;
+  long long sweep_subset = 256;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
     if (k == "--model") model_p = v;
@@ -67,6 +72,9 @@ int main(int argc, char** argv) {
     else if (k == "--anchor") cfg.ttft_anchor = v == "admission" ? TtftAnchor::Admission : TtftAnchor::Arrival;
     else if (k == "--jobs") jobs = std::stoi(v);
     else if (k == "--drop-table") drop = v;
+    else if (k == "--single") single = std::stoi(v);
+    else if (k == "--sweep-segments") sweep_segments = std::stoi(v);
+    else if (k == "--sweep-subset") sweep_subset = std::stoll(v);
   }
   try {
     const ModelSpec model = parse_model_config_file(model_p);
@@ -144,12 +152,56 @@ int main(int argc, char** argv) {
         }
       }
     }
+    size_t n_iter = 0, n_rows = 0;
+    if (single >= 0 && size_t(single) < plans.size()) {
+      const ExecutionPlan& plan = plans[size_t(single)];
+      SimConfig ec = cfg;
+      ec.emit_iterations = true;
+      if (!freqs.empty()) ec.freq_ghz = freqs.front();
+      const SimulationReport ra = simulate_plan(plan, model, cluster, trace, ref_store, ec);
+      const SimulationReport rb = plansim_gpu::simulate_plan(plan, model, cluster, trace, gpu_store, ec);
+      n_iter = ra.iterations.size();
+      if (ra.e2e_latency != rb.e2e_latency || ra.total_energy != rb.total_energy ||
+          ra.num_iterations != rb.num_iterations || ra.per_request.size() != rb.per_request.size())
+        miss("simulate_plan report");
+      if (ra.iterations.size() != rb.iterations.size()) {
+        miss("iteration count");
+      } else {
+        for (size_t k = 0; k < ra.iterations.size(); ++k) {
+          const auto& x = ra.iterations[k];
+          const auto& y = rb.iterations[k];
+          if (x.clock_start != y.clock_start || x.duration != y.duration || x.energy != y.energy ||
+              x.batch_size != y.batch_size || x.stage_seconds != y.stage_seconds ||
+              x.stage_joules != y.stage_joules) {
+            miss("iteration record " + std::to_string(k));
+            break;
+          }
+        }
+      }
+      if (sweep_segments > 0) {
+        SimConfig sc = cfg;
+        if (!freqs.empty()) sc.freq_ghz = freqs.front();
+        const SweepTable ta = sweep_max_batch(plan, model, cluster, trace, ref_store, sc,
+                                              sweep_segments, sweep_subset);
+        const SweepTable tb = plansim_gpu::sweep_max_batch(plan, model, cluster, trace, gpu_store, sc,
+                                                           sweep_segments, sweep_subset);
+        n_rows = ta.rows.size();
+        bool same = ta.observed_max_batch == tb.observed_max_batch && ta.rows.size() == tb.rows.size();
+        for (size_t k = 0; same && k < ta.rows.size(); ++k)
+          same = ta.rows[k].max_batch_size == tb.rows[k].max_batch_size &&
+                 ta.rows[k].mean_tpot == tb.rows[k].mean_tpot &&
+                 ta.rows[k].mean_ttft == tb.rows[k].mean_ttft &&
+                 ta.rows[k].e2e_latency == tb.rows[k].e2e_latency;
+        if (!same) miss("sweep table");
+      }
+    }
     const auto wa = ref_store.warnings(), wb = gpu_store.warnings();
     const std::set<std::string> sa(wa.begin(), wa.end()), sb(wb.begin(), wb.end());
     if (sa != sb) miss("clamp warnings");
     std::printf("{\"entries\":%zu,\"mismatches\":%d,\"first\":\"%s\",\"warnings\":%zu,"
+                "\"iterations\":%zu,\"sweep_rows\":%zu,"
                 "\"ref_s\":%.6f,\"gpu_s\":%.6f,\"best\":\"%s\"}\n",
-                a.entries.size(), bad, first.c_str(), sa.size(),
+                a.entries.size(), bad, first.c_str(), sa.size(), n_iter, n_rows,
                 std::chrono::duration<double>(t1 - t0).count(),
                 std::chrono::duration<double>(t2 - t1).count(),
                 a.entries.empty() ? "" : a.entries.front().report.plan_encoding.c_str());

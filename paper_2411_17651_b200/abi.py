@@ -65,7 +65,8 @@ class ConfigC(C.Structure):
                 ("chunk_size", C.c_int64), ("max_batch_size", C.c_int64),
                 ("ttft_anchor", C.c_int32), ("n_freqs", C.c_int32),
                 ("freqs", _f64p), ("detail", C.c_int32), ("rank", C.c_int32),
-                ("n_entry_subset", C.c_int32), ("entry_subset", _i32p)]
+                ("n_entry_subset", C.c_int32), ("entry_subset", _i32p),
+                ("entry_max_batch_size", _i64p), ("emit_iterations", C.c_int32)]
 
 
 ENTRY_DTYPE = np.dtype([
@@ -78,6 +79,8 @@ ENTRY_DTYPE = np.dtype([
     ("rejected_offset", "<i8")])
 METRICS_DTYPE = np.dtype([("id", "<i8"), ("ttft", "<f8"), ("tpot", "<f8"),
                           ("e2e", "<f8"), ("gen_len", "<i8")])
+ITERATION_DTYPE = np.dtype([("clock_start", "<f8"), ("duration", "<f8"), ("energy", "<f8"),
+                            ("batch_size", "<i8")])
 RANK_KEY_DTYPE = np.dtype([("num_rejected", "<i8"), ("objective_metric", "<f8"),
                            ("other_metric", "<f8"), ("enc_rank", "<i4"), ("pad_", "<i4"),
                            ("freq_ghz", "<f8"), ("entry_index", "<i8")])
@@ -93,7 +96,9 @@ class ResultC(C.Structure):
                 ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_sim", C.c_double),
                 ("ms_reduce", C.c_double), ("ms_d2h", C.c_double), ("h2d_bytes", C.c_int64),
                 ("d2h_bytes", C.c_int64), ("sum_batch", C.c_int64), ("admissions", C.c_int64),
-                ("finishes", C.c_int64)]
+                ("finishes", C.c_int64), ("n_iterations", C.c_int64),
+                ("iterations", C.c_void_p), ("n_stages", C.c_int32),
+                ("stage_seconds", C.c_void_p), ("stage_joules", C.c_void_p)]
 
 
 EXPORTED_SYMBOLS = ("psg_version", "psg_context_create", "psg_context_destroy",

@@ -4,6 +4,7 @@
 // (/root/reference/proj/src/simulator.cpp:242-296) and simulate_plan
 // (:176-240) with the same signatures plus an optional engine handle.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 
@@ -132,10 +133,18 @@ struct TraceSoA {
 
 }  // namespace
 
-RankedPlans search(const std::vector<ExecutionPlan>& plans, const ModelSpec& /*model*/,
-                   const ClusterSpec& cluster, const Trace& trace, const ProfileStore& store,
-                   Objective objective, const std::vector<double>& frequencies,
-                   const SimConfig& cfg, int /*jobs*/, Engine* engine) {
+namespace {
+
+struct RunOpts {
+  bool rank = true, detail = true, emit = false;
+  std::vector<int32_t> subset;
+  std::vector<int64_t> caps;
+};
+
+RankedPlans run(const std::vector<ExecutionPlan>& plans, const ClusterSpec& cluster,
+                const Trace& trace, const ProfileStore& store, Objective objective,
+                const std::vector<double>& frequencies, const SimConfig& cfg, Engine* engine,
+                const RunOpts& o) {
   if (plans.empty()) throw InfeasibleError("search: no feasible plan");
   std::unique_ptr<Engine> own;
   if (!engine) {
@@ -153,8 +162,12 @@ RankedPlans search(const std::vector<ExecutionPlan>& plans, const ModelSpec& /*m
   c.ttft_anchor = cfg.ttft_anchor == TtftAnchor::Admission ? PSG_ANCHOR_ADMISSION : PSG_ANCHOR_ARRIVAL;
   c.n_freqs = int32_t(frequencies.size());
   c.freqs = frequencies.empty() ? nullptr : frequencies.data();
-  c.detail = 1;
-  c.rank = 1;
+  c.detail = o.detail ? 1 : 0;
+  c.rank = o.rank ? 1 : 0;
+  c.n_entry_subset = int32_t(o.subset.size());
+  c.entry_subset = o.subset.empty() ? nullptr : o.subset.data();
+  c.entry_max_batch_size = o.caps.empty() ? nullptr : o.caps.data();
+  c.emit_iterations = o.emit ? 1 : 0;
   psg_result* res = nullptr;
   const int rc = psg_search(engine->handle(), &soa.view(), &cl, &store.view(), &tr.view, &c, &res);
   if (rc != PSG_OK) raise(rc, psg_last_error(engine->handle()));
@@ -191,16 +204,82 @@ RankedPlans search(const std::vector<ExecutionPlan>& plans, const ModelSpec& /*m
     r.rejected_ids.assign(res->rejected_ids + e.rejected_offset,
                           res->rejected_ids + e.rejected_offset + e.num_rejected);
   }
+  if (o.emit && res->n_iterations > 0) {  // simulator.cpp:158-170, replicas in order
+    SimulationReport& r = out.entries.front().report;
+    const int S = res->n_stages;
+    r.iterations.resize(size_t(res->n_iterations));
+    for (int64_t i = 0; i < res->n_iterations; ++i) {
+      IterationRecord& it = r.iterations[size_t(i)];
+      it.clock_start = res->iterations[i].clock_start;
+      it.duration = res->iterations[i].duration;
+      it.energy = res->iterations[i].energy;
+      it.batch_size = res->iterations[i].batch_size;
+      it.stage_seconds.assign(res->stage_seconds + i * S, res->stage_seconds + (i + 1) * S);
+      it.stage_joules.assign(res->stage_joules + i * S, res->stage_joules + (i + 1) * S);
+    }
+  }
   psg_result_free(res);
   return out;
 }
 
-SimulationReport simulate_plan(const ExecutionPlan& plan, const ModelSpec& model,
+}  // namespace
+
+RankedPlans search(const std::vector<ExecutionPlan>& plans, const ModelSpec& /*model*/,
+                   const ClusterSpec& cluster, const Trace& trace, const ProfileStore& store,
+                   Objective objective, const std::vector<double>& frequencies,
+                   const SimConfig& cfg, int /*jobs*/, Engine* engine) {
+  return run(plans, cluster, trace, store, objective, frequencies, cfg, engine, RunOpts{});
+}
+
+SimulationReport simulate_plan(const ExecutionPlan& plan, const ModelSpec& /*model*/,
                                const ClusterSpec& cluster, const Trace& trace,
                                const ProfileStore& store, const SimConfig& cfg, Engine* engine) {
+  // simulator.cpp:179-180: cfg.freq_ghz > 0 ? cfg.freq_ghz : device max
   const double f = cfg.freq_ghz > 0 ? cfg.freq_ghz : cluster.device.max_frequency();
-  RankedPlans r = search({plan}, model, cluster, trace, store, Objective::Latency, {f}, cfg, 1, engine);
+  RunOpts o;
+  o.rank = false;
+  o.emit = cfg.emit_iterations;
+  RankedPlans r = run({plan}, cluster, trace, store, Objective::Latency, {f}, cfg, engine, o);
   return std::move(r.entries.front().report);
+}
+
+SweepTable sweep_max_batch(const ExecutionPlan& plan, const ModelSpec& model,
+                           const ClusterSpec& cluster, const Trace& trace,
+                           const ProfileStore& store, const SimConfig& cfg, int segments,
+                           int64_t subset_size, Engine* engine) {
+  // simulator.cpp:298-329
+  if (segments < 1) throw DataError("sweep: segments must be >= 1");
+  std::unique_ptr<Engine> own;
+  if (!engine) {
+    own = std::make_unique<Engine>(0);
+    engine = own.get();
+  }
+  Trace subset;
+  const size_t take = std::min(trace.requests.size(), size_t(std::max<int64_t>(1, subset_size)));
+  subset.requests.assign(trace.requests.begin(), trace.requests.begin() + long(take));
+  SimConfig probe_cfg = cfg;
+  probe_cfg.policy.max_batch_size = 0;
+  probe_cfg.emit_iterations = false;
+  const SimulationReport probe = simulate_plan(plan, model, cluster, subset, store, probe_cfg, engine);
+  SweepTable table;
+  table.observed_max_batch = std::max<int64_t>(1, probe.max_batch_observed);
+  RunOpts o;
+  o.rank = false;
+  o.detail = false;
+  for (int i = 1; i <= segments; ++i) {
+    o.caps.push_back(std::max<int64_t>(
+        1, llround(double(i) * double(table.observed_max_batch) / segments)));
+    o.subset.push_back(0);
+  }
+  const double f = cfg.freq_ghz > 0 ? cfg.freq_ghz : cluster.device.max_frequency();
+  SimConfig run_cfg = cfg;
+  run_cfg.emit_iterations = false;
+  const RankedPlans r = run({plan}, cluster, trace, store, Objective::Latency, {f}, run_cfg, engine, o);
+  for (int i = 0; i < segments; ++i) {
+    const SimulationReport& rep = r.entries[size_t(i)].report;
+    table.rows.push_back({o.caps[size_t(i)], rep.mean_tpot, rep.mean_ttft, rep.e2e_latency});
+  }
+  return table;
 }
 
 }  // namespace psb

@@ -110,6 +110,13 @@ struct SimParams {
   uint32_t* clamp_curve;     // per curve, bit 0 below / bit 1 above
   // scratch (global fallback for large batches)
   unsigned long long* prof;  // PSG_PHASE_PROFILE builds: kProfSlots counters per unit
+  const int64_t* entry_max_bs;  // per-entry max_batch_size override, or null
+  // emit_iterations: one record + emit_S stage seconds / joules per iteration
+  // at emit_off[unit] + n; null when off (macro-stepping on)
+  psg_iteration* emit_it;
+  double *emit_sec, *emit_jou;
+  const int64_t* emit_off;
+  int32_t emit_S;
   int32_t* g_i32;            // kGI32 int32 arrays per unit, stride n_req
   double* g_f64;             // kGF64 8-byte arrays per unit, stride n_req
   int64_t* g_cm;             // per-unit chunk minima once the active slots live in global memory

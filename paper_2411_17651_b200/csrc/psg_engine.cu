@@ -128,7 +128,8 @@ struct psg_context {
   cudaEvent_t ev[8] = {};
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
-  HostBuf h_in, h_out, h_pr, h_rj;
+  HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
+  DevBuf d_it, d_isec, d_ijou, d_ioff;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
   std::vector<uint8_t> compute_clamp, curve_clamp;
@@ -185,9 +186,11 @@ void psg_context_destroy(psg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
-                    &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof})
+                    &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
+                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff})
     b->release();
-  for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj}) b->release();
+  for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj, &ctx->h_it, &ctx->h_isec, &ctx->h_ijou})
+    b->release();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -245,6 +248,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     std::iota(ent.begin(), ent.end(), 0);
   }
   const int E = int(ent.size());
+  if (cfg->emit_iterations && E != 1)
+    return fail(ctx, PSG_ERR_USAGE, "emit_iterations requires exactly one (plan, frequency) entry");
 
   // ---- validate plans ----
   const int np = P->n_plans;
@@ -548,6 +553,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
                o_eu = pk.add(entry_units.data(), entry_units.size()),
                o_epeak = pk.add(entry_peak.data(), E), o_eenc = pk.add(entry_enc.data(), E),
                o_efreq = pk.add(entry_freq.data(), E), o_eglob = pk.add(ent.data(), E);
+  const size_t o_pmb = cfg->entry_max_batch_size ? pk.add(cfg->entry_max_batch_size, size_t(E)) : 0;
   const size_t o_sgt = pk.add(sig_table.data(), sig_table.size()),
                o_sgo = pk.add(sig_op.data(), sig_op.size()),
                o_sgs = pk.add(sig_scale.data(), sig_scale.size()),
@@ -618,6 +624,11 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.entry_missing = (const int32_t*)D(o_emiss);
   sp.n_cells_total = n_cells;
   sp.units = (const Unit*)D(o_units);
+  sp.entry_max_bs = cfg->entry_max_batch_size ? (const int64_t*)D(o_pmb) : nullptr;
+  sp.emit_it = nullptr;
+  sp.emit_sec = sp.emit_jou = nullptr;
+  sp.emit_off = nullptr;
+  sp.emit_S = 0;
   sp.n_units = n_units;
   sp.batch_mode = cfg->batch_mode;
   sp.chunk_size = cfg->chunk_size;
@@ -694,6 +705,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.clamp_curve = (uint32_t*)W(w_kc);
   sp.prof = nullptr;
   const char* prof_path = std::getenv("PSG_PHASE_PROFILE");
+  if (prof_path && !*prof_path) prof_path = nullptr;
   if (prof_path) {  // dev builds: per-unit phase counters dumped after the run
     PSG_CUDA(ctx->d_prof.ensure(sizeof(unsigned long long) * kProfSlots * std::max(n_units, 1)));
     PSG_CUDA(cudaMemsetAsync(ctx->d_prof.p, 0, sizeof(unsigned long long) * kProfSlots * std::max(n_units, 1), ctx->stream));
@@ -747,6 +759,46 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
     ++launches;
     PSG_CUDA(cudaGetLastError());
+  }
+  int64_t n_emit = 0;
+  int emit_S = 0;
+  if (cfg->emit_iterations && n_units > 0) {
+    // Second pass without macro-stepping, one record per iteration; the
+    // first pass sized the log exactly (per-unit iteration counts).
+    std::vector<UnitOut> uo(n_units);
+    PSG_CUDA(cudaMemcpyAsync(uo.data(), sp.uout, n_units * sizeof(UnitOut), cudaMemcpyDeviceToHost, st));
+    PSG_CUDA(cudaStreamSynchronize(st));
+    bool failed = false;
+    for (const UnitOut& u : uo) failed |= u.err != 0;
+    if (!failed) {
+      std::vector<int64_t> off(n_units, 0);
+      for (int k = entry_unit_begin[0]; k < entry_unit_begin[1]; ++k) {  // replica order
+        off[entry_units[k]] = n_emit;
+        n_emit += uo[entry_units[k]].iterations;
+      }
+      emit_S = P->num_stages[ent[0] / F];
+      const int64_t nr = std::max<int64_t>(n_emit, 1);
+      PSG_CUDA(ctx->d_it.ensure(nr * sizeof(psg_iteration)));
+      PSG_CUDA(ctx->d_isec.ensure(nr * emit_S * sizeof(double)));
+      PSG_CUDA(ctx->d_ijou.ensure(nr * emit_S * sizeof(double)));
+      PSG_CUDA(ctx->d_ioff.ensure(n_units * sizeof(int64_t)));
+      PSG_CUDA(cudaMemcpyAsync(ctx->d_ioff.p, off.data(), n_units * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      sp.emit_it = static_cast<psg_iteration*>(ctx->d_it.p);
+      sp.emit_sec = static_cast<double*>(ctx->d_isec.p);
+      sp.emit_jou = static_cast<double*>(ctx->d_ijou.p);
+      sp.emit_off = static_cast<const int64_t*>(ctx->d_ioff.p);
+      sp.emit_S = emit_S;
+      sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
+      ++launches;
+      PSG_CUDA(cudaGetLastError());
+      // the stepwise pass is a replay: the first pass's outputs are rewritten bit-identically
+      PSG_CUDA(cudaStreamSynchronize(st));
+      PSG_CUDA(cudaMemcpyAsync(uo.data(), sp.uout, n_units * sizeof(UnitOut), cudaMemcpyDeviceToHost, st));
+      PSG_CUDA(cudaStreamSynchronize(st));
+      int64_t n2 = 0;
+      for (const UnitOut& u : uo) n2 += u.iterations;
+      if (n2 != n_emit) return fail(ctx, PSG_ERR_CUDA, "iteration log: replay diverged");
+    }
   }
   PSG_CUDA(cudaEventRecord(ctx->ev[2], st));
   entry_reduce_kernel<<<E, 256, 0, st>>>(rp);
@@ -812,6 +864,16 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     if (n_rj)
       PSG_CUDA(cudaMemcpyAsync(ctx->h_rj.p, ctx->d_rj.p, n_rj * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, st));
+  }
+  if (n_emit > 0) {
+    PSG_CUDA(ctx->h_it.ensure(n_emit * sizeof(psg_iteration)));
+    PSG_CUDA(ctx->h_isec.ensure(n_emit * emit_S * sizeof(double)));
+    PSG_CUDA(ctx->h_ijou.ensure(n_emit * emit_S * sizeof(double)));
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_it.p, ctx->d_it.p, n_emit * sizeof(psg_iteration), cudaMemcpyDeviceToHost, st));
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_isec.p, ctx->d_isec.p, n_emit * emit_S * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_ijou.p, ctx->d_ijou.p, n_emit * emit_S * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
   }
   PSG_CUDA(cudaEventRecord(ctx->ev[7], st));
   PSG_CUDA(cudaStreamSynchronize(st));
@@ -883,9 +945,15 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   res->sum_batch = sb;
   res->admissions = adm;
   res->finishes = fin;
+  res->n_iterations = n_emit;
+  res->iterations = n_emit ? static_cast<psg_iteration*>(ctx->h_it.p) : nullptr;
+  res->n_stages = emit_S;
+  res->stage_seconds = n_emit ? static_cast<double*>(ctx->h_isec.p) : nullptr;
+  res->stage_joules = n_emit ? static_cast<double*>(ctx->h_ijou.p) : nullptr;
   res->h2d_bytes = int64_t(in_bytes);
   res->d2h_bytes = int64_t(wk.size) + n_pr * int64_t(sizeof(psg_request_metrics)) +
-                   n_rj * int64_t(sizeof(int64_t));
+                   n_rj * int64_t(sizeof(int64_t)) +
+                   n_emit * int64_t(sizeof(psg_iteration) + 2 * sizeof(double) * emit_S);
   float a = 0, b = 0;
   cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
   res->ms_h2d = a;

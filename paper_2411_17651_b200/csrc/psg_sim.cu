@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   const size_t slot_base = size_t(U.entry) * size_t(p.n_slots);
   const bool chunked = p.batch_mode == PSG_BATCH_CHUNKED;
   const int64_t chunk = p.chunk_size;
-  const int64_t max_bs = p.max_batch_size;
+  const int64_t max_bs = p.entry_max_bs ? p.entry_max_bs[U.entry] : p.max_batch_size;
+  const bool stepwise = p.emit_it != nullptr;  // iteration records: no macro-stepping
   const bool chunk_err = chunked && chunk < 1;
   const bool missing = p.entry_missing[U.entry] != 0;
 
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     if (missing) { err = 2; break; }
 
     bool settle = true;
-    if (n_pre > 0) {
+    if (n_pre > 0 || stepwise) {
       // ---- mixed iteration (batching.cpp:62-108): prefill items from the
       // prefill frontier, decode count = the rest ----
       PROF_CNT(10);
@@ -641,6 +642,29 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       }
       const double cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
       const double cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
+      if (stepwise) {  // IterationRecord (simulator.cpp:158-170)
+        const int64_t r = p.emit_off[blockIdx.x] + n;
+        if (lane == 0) {
+          psg_iteration it;
+          it.clock_start = clock;
+          it.duration = cd;
+          it.energy = ce;
+          it.batch_size = B;
+          p.emit_it[r] = it;
+        }
+        double* sv = p.emit_sec + r * int64_t(p.emit_S);
+        double* jv = p.emit_jou + r * int64_t(p.emit_S);
+        for (int st = lane; st < S; st += kWarp) {
+          double sec = srep, jou = jrep;  // stage s: block * reps, + p2p of boundary s-1
+          if (st > 0 && st - 1 < NB) {
+            const int sl = p2p_slot[st - 1];
+            sec = __dadd_rn(srep, p2p_val[sl]);
+            jou = __dadd_rn(jrep, p2p_val[kMaxClampSlots + sl]);
+          }
+          sv[st] = sec;
+          jv[st] = jou;
+        }
+      }
       PROF_ADD(2, t_ev);
 
       // ---- advance (batching.cpp:78-93) over the prefill frontier ----

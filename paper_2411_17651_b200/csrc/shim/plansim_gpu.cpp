@@ -231,12 +231,18 @@ struct FlatPlans {
 
 }  // namespace
 
-plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
-                            const plansim::ModelSpec& /*model*/,
-                            const plansim::ClusterSpec& cluster, const plansim::Trace& trace,
-                            const plansim::ProfileStore& store, plansim::Objective objective,
-                            const std::vector<double>& frequencies,
-                            const plansim::SimConfig& cfg, int /*jobs*/, int device) {
+namespace {
+
+// One psg_search call.  subset / caps: optional repeated entry list with
+// per-entry max_batch_size (sweeps); emit: IterationRecords into the single
+// entry's report.
+plansim::RankedPlans run(const std::vector<plansim::ExecutionPlan>& plans,
+                         const plansim::ClusterSpec& cluster, const plansim::Trace& trace,
+                         const plansim::ProfileStore& store, plansim::Objective objective,
+                         const std::vector<double>& frequencies, const plansim::SimConfig& cfg,
+                         int device, bool rank, bool detail, bool emit,
+                         const std::vector<int32_t>& subset = {},
+                         const std::vector<int64_t>& caps = {}) {
   using namespace plansim;
   if (plans.empty()) throw InfeasibleError("search: no feasible plan");
   const FlatPlans fp(plans);
@@ -267,8 +273,12 @@ plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
   c.ttft_anchor = cfg.ttft_anchor == TtftAnchor::Admission ? PSG_ANCHOR_ADMISSION : PSG_ANCHOR_ARRIVAL;
   c.n_freqs = int32_t(frequencies.size());
   c.freqs = frequencies.empty() ? nullptr : frequencies.data();
-  c.detail = 1;
-  c.rank = 1;
+  c.detail = detail ? 1 : 0;
+  c.rank = rank ? 1 : 0;
+  c.n_entry_subset = int32_t(subset.size());
+  c.entry_subset = subset.empty() ? nullptr : subset.data();
+  c.entry_max_batch_size = caps.empty() ? nullptr : caps.data();
+  c.emit_iterations = emit ? 1 : 0;
   psg_context* h = context_for(device);
   psg_result* res = nullptr;
   const int rc = psg_search(h, &fp.v, &cl, &fs.v, &tr, &c, &res);
@@ -304,8 +314,33 @@ plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
     r.rejected_ids.assign(res->rejected_ids + e.rejected_offset,
                           res->rejected_ids + e.rejected_offset + e.num_rejected);
   }
+  if (emit && res->n_iterations > 0) {  // simulator.cpp:158-170
+    SimulationReport& r = out.entries.front().report;
+    const int S = res->n_stages;
+    r.iterations.resize(size_t(res->n_iterations));
+    for (int64_t i = 0; i < res->n_iterations; ++i) {
+      IterationRecord& it = r.iterations[size_t(i)];
+      it.clock_start = res->iterations[i].clock_start;
+      it.duration = res->iterations[i].duration;
+      it.energy = res->iterations[i].energy;
+      it.batch_size = res->iterations[i].batch_size;
+      it.stage_seconds.assign(res->stage_seconds + i * S, res->stage_seconds + (i + 1) * S);
+      it.stage_joules.assign(res->stage_joules + i * S, res->stage_joules + (i + 1) * S);
+    }
+  }
   psg_result_free(res);
   return out;
+}
+
+}  // namespace
+
+plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
+                            const plansim::ModelSpec& /*model*/,
+                            const plansim::ClusterSpec& cluster, const plansim::Trace& trace,
+                            const plansim::ProfileStore& store, plansim::Objective objective,
+                            const std::vector<double>& frequencies,
+                            const plansim::SimConfig& cfg, int /*jobs*/, int device) {
+  return run(plans, cluster, trace, store, objective, frequencies, cfg, device, true, true, false);
 }
 
 plansim::SimulationReport simulate_plan(const plansim::ExecutionPlan& plan,
@@ -316,9 +351,48 @@ plansim::SimulationReport simulate_plan(const plansim::ExecutionPlan& plan,
                                         const plansim::SimConfig& cfg, int device) {
   // simulator.cpp:180-181: cfg.freq_ghz > 0 ? cfg.freq_ghz : device max
   const double f = cfg.freq_ghz > 0 ? cfg.freq_ghz : cluster.device.max_frequency();
-  auto r = search({plan}, model, cluster, trace, store, plansim::Objective::Latency, {f}, cfg, 1,
-                  device);
+  (void)model;
+  auto r = run({plan}, cluster, trace, store, plansim::Objective::Latency, {f}, cfg, device, false,
+               true, cfg.emit_iterations);
   return std::move(r.entries.front().report);
+}
+
+plansim::SweepTable sweep_max_batch(const plansim::ExecutionPlan& plan,
+                                    const plansim::ModelSpec& model,
+                                    const plansim::ClusterSpec& cluster,
+                                    const plansim::Trace& trace,
+                                    const plansim::ProfileStore& store,
+                                    const plansim::SimConfig& cfg, int segments,
+                                    int64_t subset_size, int device) {
+  using namespace plansim;
+  // simulator.cpp:298-329: uncapped probe on the first subset_size requests,
+  // then `segments` capped runs of the whole trace — one launch here.
+  if (segments < 1) throw DataError("sweep: segments must be >= 1");
+  Trace subset;
+  subset.metadata = trace.metadata;
+  const size_t take =
+      std::min(trace.requests.size(), size_t(std::max<int64_t>(1, subset_size)));
+  subset.requests.assign(trace.requests.begin(), trace.requests.begin() + long(take));
+  SimConfig probe_cfg = cfg;
+  probe_cfg.policy.max_batch_size = 0;
+  probe_cfg.emit_iterations = false;
+  const SimulationReport probe = simulate_plan(plan, model, cluster, subset, store, probe_cfg, device);
+  SweepTable table;
+  table.observed_max_batch = std::max<int64_t>(1, probe.max_batch_observed);
+  std::vector<int64_t> caps;
+  for (int i = 1; i <= segments; ++i)
+    caps.push_back(std::max<int64_t>(
+        1, llround(double(i) * double(table.observed_max_batch) / segments)));
+  const double f = cfg.freq_ghz > 0 ? cfg.freq_ghz : cluster.device.max_frequency();
+  SimConfig run_cfg = cfg;
+  run_cfg.emit_iterations = false;
+  const auto r = run({plan}, cluster, trace, store, Objective::Latency, {f}, run_cfg, device, false,
+                     false, false, std::vector<int32_t>(size_t(segments), 0), caps);
+  for (int i = 0; i < segments; ++i) {
+    const SimulationReport& rep = r.entries[size_t(i)].report;
+    table.rows.push_back({caps[size_t(i)], rep.mean_tpot, rep.mean_ttft, rep.e2e_latency});
+  }
+  return table;
 }
 
 }  // namespace plansim_gpu

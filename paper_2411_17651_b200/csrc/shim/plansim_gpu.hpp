@@ -5,8 +5,10 @@
 // (same arguments, same RankedPlans result, same exceptions).  See
 // INTEGRATION.md.
 //
-// Replaces: plansim::search        include/plansim/simulator.hpp:99-103
-//           plansim::simulate_plan include/plansim/simulator.hpp:80-82
+// Replaces: plansim::search          include/plansim/simulator.hpp:99-103
+//           plansim::simulate_plan   include/plansim/simulator.hpp:80-82
+//                                    (emit_iterations included)
+//           plansim::sweep_max_batch include/plansim/simulator.hpp:117-122
 #pragma once
 
 #include <vector>
@@ -32,5 +34,14 @@ plansim::SimulationReport simulate_plan(const plansim::ExecutionPlan& plan,
                                         const plansim::Trace& trace,
                                         const plansim::ProfileStore& store,
                                         const plansim::SimConfig& cfg, int device = 0);
+
+// All `segments` capped simulations run in one launch.
+plansim::SweepTable sweep_max_batch(const plansim::ExecutionPlan& plan,
+                                    const plansim::ModelSpec& model,
+                                    const plansim::ClusterSpec& cluster,
+                                    const plansim::Trace& trace,
+                                    const plansim::ProfileStore& store,
+                                    const plansim::SimConfig& cfg, int segments,
+                                    int64_t subset_size = 256, int device = 0);
 
 }  // namespace plansim_gpu

@@ -10,6 +10,7 @@ Everything runs through the C ABI of libpsg.so (include/psg.h).
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 
@@ -45,6 +46,13 @@ class SearchResult:
         self.admissions = int(res.admissions)
         self.finishes = int(res.finishes)
         self.encodings = encodings
+        # emit_iterations: IterationRecord scalars + [n, stages] stage vectors
+        S = int(res.n_stages)
+        self.iterations = view(res.iterations, res.n_iterations, abi.ITERATION_DTYPE)
+        self.stage_seconds = view(res.stage_seconds, res.n_iterations * S,
+                                  np.dtype("<f8")).reshape(-1, max(S, 1))
+        self.stage_joules = view(res.stage_joules, res.n_iterations * S,
+                                 np.dtype("<f8")).reshape(-1, max(S, 1))
 
     def __len__(self):
         return len(self.entries)
@@ -58,6 +66,22 @@ class SearchResult:
 
     def encoding(self, k: int) -> str:
         return self.encodings[int(self.entries[k]["plan_index"])]
+
+
+class _TracePrefix:
+    """The first n requests of a trace (trace order, simulator.cpp:306-308) as
+    a view over the same arrays."""
+
+    def __init__(self, trace, n):
+        self._owner = trace
+        s = abi.TraceC()
+        for name, _ in abi.TraceC._fields_:
+            setattr(s, name, getattr(trace.struct, name))
+        s.n = int(n)
+        self.struct = s
+
+    def __len__(self):
+        return int(self.struct.n)
 
 
 class Engine:
@@ -102,3 +126,42 @@ class Engine:
         if rc != abi.PSG_OK:
             raise from_code(rc, self.lib.psg_last_error(self.handle).decode())
         return order
+
+    def simulate_plan(self, plans: Plans, plan_index: int, cluster: Cluster, store: Store,
+                      trace: Trace, config: Config | None = None, freq_ghz: float = 0.0,
+                      emit_iterations: bool = False) -> SearchResult:
+        """plansim::simulate_plan (simulator.cpp:176-240) for plans[plan_index]
+        at freq_ghz (0 = the device's max frequency, :179-180): a one-entry
+        search.  emit_iterations fills .iterations / .stage_* with one
+        IterationRecord per iteration (:158-170), replicas in order."""
+        a = (config or Config()).args
+        cfg = Config(freqs=[freq_ghz] if freq_ghz > 0 else [], detail=True, rank=False,
+                     entry_subset=[int(plan_index)], emit_iterations=emit_iterations, **a)
+        return self.search(plans, cluster, store, trace, cfg)
+
+    def sweep_max_batch(self, plans: Plans, plan_index: int, cluster: Cluster, store: Store,
+                        trace: Trace, config: Config | None = None, segments: int = 4,
+                        subset_size: int = 256, freq_ghz: float = 0.0) -> dict:
+        """plansim::sweep_max_batch (simulator.cpp:298-329): an uncapped probe
+        on the first subset_size requests, then `segments` capped simulations of
+        the whole trace — all caps in one launch (a repeated entry_subset with
+        per-entry max_batch_size)."""
+        if segments < 1:
+            raise from_code(abi.PSG_ERR_DATA, "sweep: segments must be >= 1")
+        a = dict((config or Config()).args)
+        take = min(len(trace), max(1, int(subset_size)))
+        sub = _TracePrefix(trace, take)
+        a["max_batch_size"] = 0
+        probe = self.simulate_plan(plans, plan_index, cluster, store, sub, Config(**a), freq_ghz)
+        observed = max(1, int(probe.entries[0]["max_batch_observed"]))
+        caps = []
+        for i in range(1, segments + 1):
+            x = float(i) * float(observed) / float(segments)  # llround, half away from zero
+            r = math.floor(x)
+            caps.append(max(1, int(r) + (1 if x - r >= 0.5 else 0)))
+        cfg = Config(freqs=[freq_ghz] if freq_ghz > 0 else [], detail=False, rank=False,
+                     entry_subset=[int(plan_index)] * segments, entry_max_batch_size=caps, **a)
+        res = self.search(plans, cluster, store, trace, cfg)
+        rows = [(caps[k], float(res.entries[k]["mean_tpot"]), float(res.entries[k]["mean_ttft"]),
+                 float(res.entries[k]["e2e_latency"])) for k in range(segments)]
+        return {"observed_max_batch": observed, "rows": rows}

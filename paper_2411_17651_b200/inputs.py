@@ -325,10 +325,12 @@ ANCHOR = {"arrival": 0, "admission": 1}
 class Config:
     def __init__(self, objective="latency", freqs=(), batching="contiguous", chunk_size=256,
                  max_batch_size=0, ttft_anchor="arrival", detail=True, rank=True,
-                 entry_subset=None):
+                 entry_subset=None, entry_max_batch_size=None, emit_iterations=False):
         self.freqs = np.ascontiguousarray(list(freqs) or [0.0], dtype=np.float64)
         self.subset = np.ascontiguousarray(entry_subset if entry_subset is not None else [0],
                                            dtype=np.int32)
+        self.caps = (np.ascontiguousarray(entry_max_batch_size, dtype=np.int64)
+                     if entry_max_batch_size is not None else None)
         s = abi.ConfigC()
         s.objective = OBJECTIVE[objective]
         s.batch_mode = BATCHING[batching]
@@ -341,4 +343,9 @@ class Config:
         s.rank = int(bool(rank))
         s.n_entry_subset = 0 if entry_subset is None else len(entry_subset)
         s.entry_subset = self.subset.ctypes.data_as(C.POINTER(C.c_int32))
+        s.entry_max_batch_size = (self.caps.ctypes.data_as(C.POINTER(C.c_int64))
+                                  if self.caps is not None else None)
+        s.emit_iterations = int(bool(emit_iterations))
         self.struct = s
+        self.args = dict(objective=objective, batching=batching, chunk_size=chunk_size,
+                         max_batch_size=max_batch_size, ttft_anchor=ttft_anchor)

@@ -2,6 +2,7 @@
 the compiled reference (refdrv), the CPU restatement oracle and the GPU engine."""
 from __future__ import annotations
 
+import json
 import os
 
 import numpy as np
@@ -38,8 +39,7 @@ class Case:
         p = self.prob
         return engine.search(p.plans, p.cluster, p.store, p.trace, self.config(**kw))
 
-    def reference(self, workdir, tag):
-        """Runs the compiled reference on the same files; returns its entries."""
+    def _ref_args(self, workdir, tag):
         d = os.path.join(workdir, "case_" + tag)
         os.makedirs(d, exist_ok=True)
         files = {}
@@ -64,14 +64,47 @@ class Case:
             args += ["--max-batch", c["max_batch_size"]]
         if c.get("ttft_anchor"):
             args += ["--anchor", c["ttft_anchor"]]
+        return d, args
+
+    def _plan_spec(self):
+        assert self.plan_specs is not None and len(self.plan_specs) == 1, \
+            "reference simulate runs one plan"
+        dp, pp, cells = self.plan_specs[0]
+        return ",".join([str(dp), str(pp)] + [f"{m}:{a}:{b}" for m, a, b in cells])
+
+    def reference(self, workdir, tag):
+        """Runs the compiled reference on the same files; returns its entries."""
+        d, args = self._ref_args(workdir, tag)
         if self.plan_specs is None:
             rc, line, err = pyoracle.refdrv(["search"] + args + ["--jobs", "1"])
         else:
-            assert len(self.plan_specs) == 1, "reference simulate runs one plan"
-            dp, pp, cells = self.plan_specs[0]
-            spec = ",".join([str(dp), str(pp)] + [f"{m}:{a}:{b}" for m, a, b in cells])
-            rc, line, err = pyoracle.refdrv(["simulate"] + args + ["--plan-spec", spec])
+            rc, line, err = pyoracle.refdrv(["simulate"] + args + ["--plan-spec", self._plan_spec()])
         return rc, err, (pyoracle.read_refdump(os.path.join(d, "ref.bin"))[0] if rc == 0 else None)
+
+    def reference_iterations(self, workdir, tag):
+        """simulate_plan with emit_iterations (iterations_to_jsonl records)."""
+        d, args = self._ref_args(workdir, tag)
+        path = os.path.join(d, "iterations.jsonl")
+        rc, line, err = pyoracle.refdrv(["simulate"] + args + ["--plan-spec", self._plan_spec(),
+                                                               "--emit-iterations", path])
+        if rc != 0:
+            return rc, err, None, None
+        with open(path) as f:
+            its = [json.loads(x) for x in f if x.strip()]
+        return rc, err, pyoracle.read_refdump(os.path.join(d, "ref.bin"))[0], its
+
+    def reference_sweep(self, workdir, tag, segments, subset):
+        """sweep_max_batch: (observed_max_batch, [(cap, mean_tpot, mean_ttft, e2e)])."""
+        d, args = self._ref_args(workdir, tag)
+        rc, line, err = pyoracle.refdrv(["sweep"] + args + ["--plan-spec", self._plan_spec(),
+                                                            "--segments", str(segments),
+                                                            "--subset", str(subset)])
+        if rc != 0:
+            return rc, err, None
+        doc = line
+        rows = [(int(r[0]), float.fromhex(r[1]), float.fromhex(r[2]), float.fromhex(r[3]))
+                for r in doc["rows"]]
+        return rc, err, {"observed_max_batch": doc["observed_max_batch"], "rows": rows}
 
 
 def same_as_reference(res, ref_entries, tally_rtol=0.0):

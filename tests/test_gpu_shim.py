@@ -59,3 +59,25 @@ def test_drop_in_raises_the_reference_data_error(workdir):
     args = w.refdrv_args(w.materialize(os.path.join(workdir, "shim_err"))) + ["--drop-table", "gemm"]
     rc, line, err = run(args)
     assert rc == 4 and line["error_parity"], (line, err)
+
+
+SINGLE = [
+    ("c1", ["--single", "0", "--sweep-segments", "4", "--sweep-subset", "200"]),
+    ("c1", ["--single", "7", "--sweep-segments", "5", "--sweep-subset", "64",
+            "--batching", "chunked", "--chunk", "96"]),
+    ("c4", ["--single", "3", "--sweep-segments", "3", "--sweep-subset", "128"]),
+    ("c3", ["--single", "5", "--sweep-segments", "2", "--sweep-subset", "300"]),
+]
+
+
+@needs
+@pytest.mark.parametrize("key,extra", SINGLE, ids=[k + "".join(e) for k, e in SINGLE])
+def test_drop_in_simulate_plan_iterations_and_sweep(workdir, key, extra):
+    """plansim_gpu::simulate_plan with emit_iterations (every IterationRecord)
+    and plansim_gpu::sweep_max_batch (every SweepRow) vs the reference."""
+    w = WORKLOADS[key]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shim1_" + key))) + extra
+    rc, line, err = run(args)
+    assert rc == 0, (line, err)
+    assert line["mismatches"] == 0, line
+    assert line["iterations"] > 0 and line["sweep_rows"] > 0
