@@ -379,4 +379,13 @@ SweepTable sweep_max_batch(const ExecutionPlan& plan, const ModelSpec& model,
                            const ProfileStore& store, const SimConfig& cfg, int segments,
                            int64_t subset_size = 256, Engine* engine = nullptr);
 
+// Report materialization (simulator.cpp:331-397, tools/plansim_main.cpp:
+// 128-131, :184-199): byte-identical to the reference's nlohmann output,
+// streamed without a JSON document.
+std::string report_to_json(const SimulationReport& report);
+std::string iterations_to_jsonl(const SimulationReport& report);
+std::string report_summary_line(const SimulationReport& report);
+void write_ranked_json(const RankedPlans& ranked, const std::string& path);  // CLI ranked.json
+std::string sweep_to_json(const SweepTable& table);                          // CLI sweep --out
+
 }  // namespace psb

@@ -61,6 +61,29 @@ char* psgh_store_serialize(const psgh_problem* p);
 char* psgh_trace_serialize(const psgh_problem* p);
 void psgh_string_free(char* s);
 
+/* Report materialization over psg_search results: streams the reference
+   CLI's ranked.json (tools/plansim_main.cpp:128-131: the array of
+   report_to_json objects, simulator.cpp:331-369, dumped with indent 2)
+   byte for byte, without building a JSON document.  entries in output order
+   (ranked), per_request / rejected_ids addressed by the entries' offsets,
+   plan_encodings indexed by psg_entry.plan_index. */
+int psgh_write_ranked_json(const psg_entry* entries, int64_t n_entries,
+                           const psg_request_metrics* per_request, const int64_t* rejected_ids,
+                           const char* const* plan_encodings, int32_t n_plans, const char* path);
+/* The CLI's simulate --out report (report_to_json of one entry; iterations go
+   to the JSONL stream, tools/plansim_main.cpp:166-171). */
+int psgh_write_report_json(const psg_entry* entry, const psg_request_metrics* per_request,
+                           const int64_t* rejected_ids, const char* plan_encoding,
+                           const char* path);
+/* iterations_to_jsonl (simulator.cpp:371-385) over psg_result.iterations. */
+int psgh_write_iterations_jsonl(const psg_iteration* iterations, int64_t n,
+                                const double* stage_seconds, const double* stage_joules,
+                                int32_t n_stages, const char* path);
+/* The CLI's sweep --out table (tools/plansim_main.cpp:184-199). */
+int psgh_write_sweep_json(int64_t observed_max_batch, const int64_t* caps, const double* mean_tpot,
+                          const double* mean_ttft, const double* e2e_latency, int32_t n_rows,
+                          const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,9 @@ struct Args {
   std::string out_result, out_plans, out_store, out_trace, emit_iterations;
   int segments = 4;
   long long subset = 256;
+  // the reference CLI's output files, produced with its own recipe
+  // (tools/plansim_main.cpp:128-131, :166-172, :184-199)
+  std::string out_ranked, out_report, out_summary, out_sweep;
 };
 
 std::vector<double> split_doubles(const std::string& s) {
@@ -117,6 +120,10 @@ Args parse(int argc, char** argv) {
     else if (k == "--out-trace") a.out_trace = v();
     else if (k == "--emit-iterations") a.emit_iterations = v();
     else if (k == "--segments") a.segments = std::stoi(v());
+    else if (k == "--out-ranked") a.out_ranked = v();
+    else if (k == "--out-report") a.out_report = v();
+    else if (k == "--out-summary") a.out_summary = v();
+    else if (k == "--out-sweep") a.out_sweep = v();
     else if (k == "--subset") a.subset = std::stoll(v());
     else throw DataError("unknown flag " + k);
   }
@@ -312,6 +319,12 @@ int run(const Args& a) {
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (!a.emit_iterations.empty())
       write_file(a.emit_iterations, iterations_to_jsonl(r));
+    if (!a.out_report.empty()) {  // cmd_simulate: records live in the JSONL stream
+      SimulationReport rr = r;
+      rr.iterations.clear();
+      write_file(a.out_report, report_to_json(rr));
+    }
+    if (!a.out_summary.empty()) write_file(a.out_summary, report_summary_line(r) + "\n");
     if (!a.out_result.empty())
       write_result(a.out_result, {{0LL, r.frequency_ghz}}, {&r}, store);
     if (!a.out_plans.empty()) write_file(a.out_plans, plans_json({plan}));
@@ -327,6 +340,17 @@ int run(const Args& a) {
     const SweepTable t =
         sweep_max_batch(plan, model, cluster, trace, store, run_cfg, a.segments, a.subset);
     if (!a.out_plans.empty()) write_file(a.out_plans, plans_json({plan}));
+    if (!a.out_sweep.empty()) {  // cmd_sweep's table
+      nlohmann::ordered_json doc;
+      doc["observed_max_batch"] = t.observed_max_batch;
+      doc["rows"] = nlohmann::ordered_json::array();
+      for (const auto& row : t.rows)
+        doc["rows"].push_back({{"max_batch_size", row.max_batch_size},
+                               {"mean_tpot_s", row.mean_tpot},
+                               {"mean_ttft_s", row.mean_ttft},
+                               {"e2e_latency_s", row.e2e_latency}});
+      write_file(a.out_sweep, doc.dump(2) + "\n");
+    }
     std::printf("{\"cmd\":\"sweep\",\"observed_max_batch\":%lld,\"rows\":[",
                 (long long)t.observed_max_batch);
     for (size_t i = 0; i < t.rows.size(); ++i)
@@ -359,6 +383,15 @@ int run(const Args& a) {
   }
   long long iters = 0;
   for (const auto& e : ranked.entries) iters += e.report.num_iterations;
+  double ranked_s = 0.0;
+  if (!a.out_ranked.empty()) {  // cmd_search's ranked.json
+    const auto t0 = std::chrono::steady_clock::now();
+    nlohmann::ordered_json doc = nlohmann::ordered_json::array();
+    for (const auto& e : ranked.entries)
+      doc.push_back(nlohmann::ordered_json::parse(report_to_json(e.report)));
+    write_file(a.out_ranked, doc.dump(2) + "\n");
+    ranked_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
   if (!a.out_result.empty()) {
     std::vector<std::pair<long long, double>> keys;
     std::vector<const SimulationReport*> reps;
@@ -371,9 +404,9 @@ int run(const Args& a) {
   std::printf(
       "{\"cmd\":\"search\",\"plans\":%zu,\"plans_total\":%zu,\"entries\":%zu,"
       "\"requests\":%zu,\"plan_iterations\":%lld,\"jobs\":%d,\"repeat\":%d,"
-      "\"search_s_best\":%.9g,\"plan_iter_per_s\":%.9g,\"best\":\"%s\"}\n",
+      "\"search_s_best\":%.9g,\"plan_iter_per_s\":%.9g,\"ranked_s\":%.9g,\"best\":\"%s\"}\n",
       plans.size(), total_plans, ranked.entries.size(), trace.requests.size(), iters,
-      a.jobs, a.repeat, best, double(iters) / best,
+      a.jobs, a.repeat, best, double(iters) / best, ranked_s,
       ranked.entries.empty() ? "" : ranked.entries.front().report.plan_encoding.c_str());
   return 0;
 }

@@ -67,6 +67,61 @@ class SearchResult:
     def encoding(self, k: int) -> str:
         return self.encodings[int(self.entries[k]["plan_index"])]
 
+    # ---- report materialization (byte-identical to the reference's JSON) ----
+    def write_ranked_json(self, path: str) -> None:
+        """The reference CLI's ranked.json (tools/plansim_main.cpp:128-131),
+        streamed by the native writer (csrc/host/report.cpp)."""
+        lib = abi.load_library()
+        enc = (C.c_char_p * max(1, len(self.encodings)))(*[e.encode() for e in self.encodings])
+        pr = np.ascontiguousarray(self.per_request)
+        rj = np.ascontiguousarray(self.rejected_ids)
+        ent = np.ascontiguousarray(self.entries)
+        rc = lib.psgh_write_ranked_json(C.c_void_p(ent.ctypes.data), C.c_int64(len(ent)),
+                                        C.c_void_p(pr.ctypes.data), C.c_void_p(rj.ctypes.data),
+                                        enc, C.c_int32(len(self.encodings)), path.encode())
+        if rc != abi.PSG_OK:
+            raise from_code(rc, f"cannot write {path}")
+
+    def write_report_json(self, k: int, path: str) -> None:
+        """report_to_json of entry k (simulator.cpp:331-369) — the CLI's
+        simulate --out file."""
+        lib = abi.load_library()
+        ent = np.ascontiguousarray(self.entries[k:k + 1])
+        pr = np.ascontiguousarray(self.per_request)
+        rj = np.ascontiguousarray(self.rejected_ids)
+        rc = lib.psgh_write_report_json(C.c_void_p(ent.ctypes.data), C.c_void_p(pr.ctypes.data),
+                                        C.c_void_p(rj.ctypes.data), self.encoding(k).encode(),
+                                        path.encode())
+        if rc != abi.PSG_OK:
+            raise from_code(rc, f"cannot write {path}")
+
+    def write_iterations_jsonl(self, path: str) -> None:
+        """iterations_to_jsonl (simulator.cpp:371-385) of an emit_iterations run."""
+        lib = abi.load_library()
+        its = np.ascontiguousarray(self.iterations)
+        sec = np.ascontiguousarray(self.stage_seconds, dtype=np.float64)
+        jou = np.ascontiguousarray(self.stage_joules, dtype=np.float64)
+        S = sec.shape[1] if len(its) else 0
+        rc = lib.psgh_write_iterations_jsonl(C.c_void_p(its.ctypes.data), C.c_int64(len(its)),
+                                             C.c_void_p(sec.ctypes.data), C.c_void_p(jou.ctypes.data),
+                                             C.c_int32(S), path.encode())
+        if rc != abi.PSG_OK:
+            raise from_code(rc, f"cannot write {path}")
+
+
+def write_sweep_json(sweep: dict, path: str) -> None:
+    """The reference CLI's sweep table (tools/plansim_main.cpp:184-199)."""
+    lib = abi.load_library()
+    rows = sweep["rows"]
+    caps = np.array([r[0] for r in rows], dtype=np.int64)
+    tpot, ttft, e2e = (np.array([r[i] for r in rows], dtype=np.float64) for i in (1, 2, 3))
+    rc = lib.psgh_write_sweep_json(C.c_int64(int(sweep["observed_max_batch"])),
+                                   C.c_void_p(caps.ctypes.data), C.c_void_p(tpot.ctypes.data),
+                                   C.c_void_p(ttft.ctypes.data), C.c_void_p(e2e.ctypes.data),
+                                   C.c_int32(len(rows)), path.encode())
+    if rc != abi.PSG_OK:
+        raise from_code(rc, f"cannot write {path}")
+
 
 class _TracePrefix:
     """The first n requests of a trace (trace order, simulator.cpp:306-308) as

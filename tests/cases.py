@@ -82,11 +82,16 @@ class Case:
         return rc, err, (pyoracle.read_refdump(os.path.join(d, "ref.bin"))[0] if rc == 0 else None)
 
     def reference_iterations(self, workdir, tag):
-        """simulate_plan with emit_iterations (iterations_to_jsonl records)."""
+        """simulate_plan with emit_iterations (iterations_to_jsonl records);
+        the CLI's report / JSONL / summary files are left in case_<tag>/."""
         d, args = self._ref_args(workdir, tag)
         path = os.path.join(d, "iterations.jsonl")
         rc, line, err = pyoracle.refdrv(["simulate"] + args + ["--plan-spec", self._plan_spec(),
-                                                               "--emit-iterations", path])
+                                                               "--emit-iterations", path,
+                                                               "--out-report",
+                                                               os.path.join(d, "report.json"),
+                                                               "--out-summary",
+                                                               os.path.join(d, "summary.txt")])
         if rc != 0:
             return rc, err, None, None
         with open(path) as f:
@@ -98,7 +103,9 @@ class Case:
         d, args = self._ref_args(workdir, tag)
         rc, line, err = pyoracle.refdrv(["sweep"] + args + ["--plan-spec", self._plan_spec(),
                                                             "--segments", str(segments),
-                                                            "--subset", str(subset)])
+                                                            "--subset", str(subset),
+                                                            "--out-sweep",
+                                                            os.path.join(d, "sweep.json")])
         if rc != 0:
             return rc, err, None
         doc = line

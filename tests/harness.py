@@ -18,7 +18,7 @@ EXACT_TALLY = ("mfu", "mbu")  # per-replica partial tallies
 
 
 class RefCase:
-    def __init__(self, key, workdir, extra=(), jobs=None):
+    def __init__(self, key, workdir, extra=(), jobs=None, out_ranked=False):
         self.key = key
         w = WORKLOADS[key]
         d = os.path.join(workdir, key + "".join(str(x) for x in extra).replace("-", "_"))
@@ -33,6 +33,9 @@ class RefCase:
         args = ["search"] + w.refdrv_args(paths) + list(extra) + [
             "--jobs", jobs, "--out-result", self.dump, "--out-plans", self.plans_path,
             "--out-store", self.store_path, "--out-trace", self.trace_path]
+        self.ranked_path = os.path.join(d, "ranked.json") if out_ranked else None
+        if out_ranked:
+            args += ["--out-ranked", self.ranked_path]
         rc, self.line, err = pyoracle.refdrv(args)
         assert rc == 0, err
         self.ref, self.warnings = pyoracle.read_refdump(self.dump)
