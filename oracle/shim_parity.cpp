@@ -2,7 +2,7 @@
 // (oracle/_ref/libplansim_ref.a) and the drop-in plansim_gpu::search
 // (paper_2411_17651_b200/csrc/shim, over libpsg.so) on the SAME in-memory
 // reference objects and compares every RankedPlans field: ranked order, all
-// SimulationReport scalars (bit-exact; MFU/MBU within 1e-9 relative), every
+// SimulationReport scalars (bit-exact, MFU/MBU included), every
 // per_request metric, rejected ids, and the store's clamp-warning set.
 //
 // usage: shim_parity --model F --cluster F (--profiles F | --synth-profiles X)
@@ -133,8 +133,7 @@ int main(int argc, char** argv) {
       if (r.e2e_latency != g.e2e_latency || r.total_energy != g.total_energy ||
           r.p95_latency != g.p95_latency || r.mean_ttft != g.mean_ttft || r.mean_tpot != g.mean_tpot)
         miss("latency/energy/ttft/tpot" + at);
-      auto close = [](double u, double v) { return u == v || std::fabs(u - v) <= 1e-9 * std::fmax(std::fabs(u), std::fabs(v)); };
-      if (!close(r.mfu, g.mfu) || !close(r.mbu, g.mbu)) miss("mfu/mbu" + at);
+      if (r.mfu != g.mfu || r.mbu != g.mbu) miss("mfu/mbu" + at);
       if (r.num_completed != g.num_completed || r.num_rejected != g.num_rejected ||
           r.num_iterations != g.num_iterations || r.max_batch_observed != g.max_batch_observed)
         miss("counters" + at);

@@ -91,6 +91,9 @@ struct SimParams {
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
   int32_t serial_run;        // decode-run iterations stepped serially before the closed form
+  int32_t chain_replicas;    // 1: grid = entries, replicas run in order with one tally
+  const int32_t* entry_unit_begin;  // [E+1] units of entry e (replica order) ...
+  const int32_t* entry_units;       // ... as unit indices
   int32_t tab_smem;          // doubles of per-unit curve staging in shared memory
   int32_t cm2_cap;           // finish-summary groups (1024 slots each) in shared memory
   // precomputed cost tables (psg_tables.cu)

@@ -636,6 +636,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.anchor = cfg->ttft_anchor;
   sp.memo_cap = 256;
   sp.tab_smem = tab_smem;
+  sp.chain_replicas = 1;
+  if (const char* v = std::getenv("PSG_CHAIN_REPLICAS")) sp.chain_replicas = std::atoi(v) != 0;  // dev knob
   {
     // Active slots live in shared memory while they fit: give each unit as
     // many as keeps every unit resident in one wave (the kernel's time is its
@@ -643,7 +645,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     int64_t max_nr = 0;
     for (const auto& u : units) max_nr = std::max<int64_t>(max_nr, u.n_req);
     const int64_t want = std::max<int64_t>(256, (max_nr + 31) / 32 * 32);
-    const int per_sm = std::max(1, (n_units + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
+    const int blocks = sp.chain_replicas ? E : n_units;
+    const int per_sm = std::max(1, (blocks + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
     const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024);
     int64_t cap = 256;
     for (int64_t c = want; c > 256; c -= 32) {
@@ -734,6 +737,9 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   rp.total_devices = cl->total_devices;
   rp.objective = cfg->objective;
   rp.extras = 1;
+  rp.chain_replicas = sp.chain_replicas;
+  sp.entry_unit_begin = rp.entry_unit_begin;
+  sp.entry_units = rp.entry_units;
   rp.eout = (EntryOut*)W(w_eout);
   rp.keys = (psg_rank_key*)W(w_keys);
 
@@ -756,7 +762,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     ++launches;
   }
   if (n_units > 0) {
-    sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
+    sim_kernel<<<sp.chain_replicas ? E : n_units, kWarp, smem, st>>>(sp);
     ++launches;
     PSG_CUDA(cudaGetLastError());
   }
@@ -788,7 +794,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
       sp.emit_jou = static_cast<double*>(ctx->d_ijou.p);
       sp.emit_off = static_cast<const int64_t*>(ctx->d_ioff.p);
       sp.emit_S = emit_S;
-      sim_kernel<<<n_units, kWarp, smem, st>>>(sp);
+      sim_kernel<<<sp.chain_replicas ? E : n_units, kWarp, smem, st>>>(sp);
       ++launches;
       PSG_CUDA(cudaGetLastError());
       // the stepwise pass is a replay: the first pass's outputs are rewritten bit-identically

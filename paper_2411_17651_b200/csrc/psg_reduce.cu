@@ -142,8 +142,13 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
       const UnitOut& u = r.uout[r.entry_units[k]];
       o.e2e = o.e2e < u.clock ? u.clock : o.e2e;
       o.energy = __dadd_rn(o.energy, u.energy);
-      o.flops = __dadd_rn(o.flops, u.flops);
-      o.bytes = __dadd_rn(o.bytes, u.bytes);
+      if (r.chain_replicas) {  // one WorkTally across replicas (simulator.cpp:195-201)
+        o.flops = u.flops;
+        o.bytes = u.bytes;
+      } else {
+        o.flops = __dadd_rn(o.flops, u.flops);
+        o.bytes = __dadd_rn(o.bytes, u.bytes);
+      }
       o.iterations += u.iterations;
       o.max_batch = o.max_batch > u.max_batch ? o.max_batch : u.max_batch;
       o.rejected += u.rejected;

@@ -34,6 +34,7 @@ struct ReduceParams {
   int32_t total_devices;
   int32_t objective;
   int32_t extras;
+  int32_t chain_replicas;  // uout flops/bytes are running tallies: take the last replica's
   EntryOut* eout;
   psg_rank_key* keys;
 };

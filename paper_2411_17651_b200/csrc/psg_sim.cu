@@ -117,16 +117,19 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
+// One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
+// carry WorkTally across the entry's replicas (simulator.cpp:195-201).
+__device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
+                                         double& tally_flops, double& tally_bytes,
+                                         unsigned char* smem_raw) {
   const int lane = threadIdx.x;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const Unit U = p.units[blockIdx.x];
+  const Unit U = p.units[unit_idx];
 #ifdef PSG_PHASE_PROFILE
   unsigned long long prof_acc[kProfSlots] = {};
   const long long prof_start = clock64();
 #endif
 
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap);
   double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
   CurveDesc* cdesc = reinterpret_cast<CurveDesc*>(smem_raw + L.cdesc);
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   // visits only the groups / chunks whose minimum is due.
   int64_t* cm1 = reinterpret_cast<int64_t*>(smem_raw + L.cm1);
   int64_t* cm2 = reinterpret_cast<int64_t*>(smem_raw + L.cm2);
-  int64_t* g_cm = p.g_cm + (U.scratch >> 5) + 2 * int64_t(blockIdx.x);
+  int64_t* g_cm = p.g_cm + (U.scratch >> 5) + 2 * int64_t(unit_idx);
 
   auto req_tidx = [&](int j) -> int {
     return p.T.seq ? p.T.seq[U.seq_base + j]
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   const bool chunk_err = chunked && chunk < 1;
   const bool missing = p.entry_missing[U.entry] != 0;
 
-  double clock = 0.0, energy = 0.0, flops = 0.0, bytes = 0.0;
+  double clock = 0.0, energy = 0.0, flops = tally_flops, bytes = tally_bytes;
   int64_t n = 0, max_batch = 0, completed = 0, rejected = 0, sum_batch = 0, admissions = 0;
   int pend = 0, stack_top = 0, w_base = -kWindow;
   // Active slots in admission order with tombstones: B live of len used;
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       const double cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
       const double cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
       if (stepwise) {  // IterationRecord (simulator.cpp:158-170)
-        const int64_t r = p.emit_off[blockIdx.x] + n;
+        const int64_t r = p.emit_off[unit_idx] + n;
         if (lane == 0) {
           psg_iteration it;
           it.clock_start = clock;
@@ -951,10 +954,12 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
 
   // ---- unit outputs ----
   __syncwarp();
+  tally_flops = flops;
+  tally_bytes = bytes;
 #ifdef PSG_PHASE_PROFILE
   prof_acc[15] = (unsigned long long)(clock64() - prof_start);
   if (lane == 0 && p.prof)
-    for (int k = 0; k < kProfSlots; ++k) p.prof[size_t(blockIdx.x) * kProfSlots + k] = prof_acc[k];
+    for (int k = 0; k < kProfSlots; ++k) p.prof[size_t(unit_idx) * kProfSlots + k] = prof_acc[k];
 #endif
   if (lane == 0) {
     UnitOut o;
@@ -970,7 +975,7 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
     o.admissions = admissions;
     o.err = err;
     o.pad = 0;
-    p.uout[blockIdx.x] = o;
+    p.uout[unit_idx] = o;
   }
   // clamp flags from the extreme queried token counts / totals: every
   // query's x is monotone in its token count (cost.cpp:85-102 locate)
@@ -1005,6 +1010,22 @@ __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
       const uint32_t bits = uint32_t(xlo < kn[0]) | uint32_t(xhi > kn[d.n - 1]) << 1;
       if (bits) atomicOr(p.clamp_curve + d.table, bits);
     }
+  }
+}
+
+__global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double tf = 0.0, tb = 0.0;
+  if (p.chain_replicas) {
+    // one warp per entry: its replicas in order, one running tally — the
+    // reference's WorkTally, so MFU / MBU are bit-exact for DP > 1
+    const int e = blockIdx.x;
+    for (int k = p.entry_unit_begin[e]; k < p.entry_unit_begin[e + 1]; ++k) {
+      sim_unit(p, p.entry_units[k], tf, tb, smem_raw);
+      __syncwarp();
+    }
+  } else {
+    sim_unit(p, blockIdx.x, tf, tb, smem_raw);
   }
 }
 

@@ -61,4 +61,4 @@ def test_oracle_matches_golden(name):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", NAMES)
 def test_engine_matches_golden(engine, name):
-    check(run(name, engine), load(name), tally_rtol=1e-9)
+    check(run(name, engine), load(name), tally_rtol=0.0)

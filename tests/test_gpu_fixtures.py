@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(catalog.NAMED))
 def test_engine_matches_oracle_on_fixture(engine, name):
     case = catalog.NAMED[name]()
-    same_results(case.gpu(engine), case.oracle(), tally_rtol=1e-9)
+    same_results(case.gpu(engine), case.oracle(), tally_rtol=0.0)
 
 
 @pytest.mark.parametrize("seed", range(200))
