@@ -279,6 +279,19 @@ int psg_search(psg_context* ctx, const psg_plan_set* plans,
                const psg_trace* trace, const psg_config* config,
                psg_result** out);
 
+/* n independent searches (e.g. the design spaces of several quantization
+   formats) run concurrently on one device, one context (stream, buffers,
+   result) each; shared memory is sized for all of them at once.  outs[i] as
+   from psg_search(ctxs[i], ...).  Returns the first failing search's code
+   (psg_last_error(ctxs[i]) says which); on failure outs of the successful
+   searches are still valid and must be freed.  kernel_span_ms (optional):
+   device time from the first search's kernels starting to the last one's
+   finishing (inputs resident, transfers excluded). */
+int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* plans,
+                    const psg_cluster* const* clusters, const psg_store* const* stores,
+                    const psg_trace* const* traces, const psg_config* const* configs,
+                    psg_result** outs, double* kernel_span_ms);
+
 /* Device ranking of gathered keys (multi-GPU merge): order[k] = index into
    keys of the k-th best entry under the comparator of simulator.cpp:283-294. */
 int psg_rank_keys(psg_context* ctx, const psg_rank_key* keys, int64_t n,

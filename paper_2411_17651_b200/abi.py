@@ -102,7 +102,8 @@ class ResultC(C.Structure):
 
 
 EXPORTED_SYMBOLS = ("psg_version", "psg_context_create", "psg_context_destroy",
-                    "psg_last_error", "psg_search", "psg_rank_keys", "psg_result_free")
+                    "psg_last_error", "psg_search", "psg_search_many", "psg_rank_keys",
+                    "psg_result_free")
 
 _lib = None
 

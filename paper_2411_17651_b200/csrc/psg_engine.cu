@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -124,6 +125,7 @@ struct psg_context {
   int device = 0;
   int n_sm = 148;                  // device properties used to size the simulation launch
   int64_t smem_sm = 228 * 1024, smem_block_max = 227 * 1024;
+  int concurrent_blocks = 0;       // psg_search_many: simulation blocks sharing the device
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
@@ -176,6 +178,9 @@ int psg_context_create(int device, psg_context** out) {
     delete ctx;
     return PSG_ERR_CUDA;
   }
+  // the cap only; each launch asks for what it needs (set once: contexts may
+  // launch concurrently from several threads)
+  cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_block_max));
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
   return PSG_OK;
@@ -645,7 +650,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     int64_t max_nr = 0;
     for (const auto& u : units) max_nr = std::max<int64_t>(max_nr, u.n_req);
     const int64_t want = std::max<int64_t>(256, (max_nr + 31) / 32 * 32);
-    const int blocks = sp.chain_replicas ? E : n_units;
+    const int blocks = std::max(sp.chain_replicas ? E : n_units, ctx->concurrent_blocks);
     const int per_sm = std::max(1, (blocks + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
     const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024);
     int64_t cap = 256;
@@ -752,7 +757,6 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
   const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem, sp.cm2_cap);
   if (prof_path) std::fprintf(stderr, "psg: units=%d smem_cap=%d smem=%zu B\n", n_units, sp.smem_cap, smem);
-  PSG_CUDA(cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (n_sig > 0) {  // cell-query tables, then decode-only iteration tables
     qtab_kernel<<<dim3(unsigned(n_sig), unsigned((max_qrows + 255) / 256)), 256, 0, st>>>(tp);
     ++launches;
@@ -973,6 +977,56 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   res->ms_d2h = double(a) + double(b);
   res->ms_total = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
   *out = res;
+  return PSG_OK;
+}
+
+int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* plans,
+                    const psg_cluster* const* clusters, const psg_store* const* stores,
+                    const psg_trace* const* traces, const psg_config* const* configs,
+                    psg_result** outs, double* kernel_span_ms) {
+  if (n <= 0 || !ctxs || !plans || !clusters || !stores || !traces || !configs || !outs)
+    return PSG_ERR_USAGE;
+  // every search's simulation blocks share the device: size shared memory so
+  // they are all resident in one wave
+  int total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || !plans[i] || !configs[i]) return PSG_ERR_USAGE;
+    for (int j = 0; j < i; ++j)
+      if (ctxs[j] == ctxs[i]) return PSG_ERR_USAGE;  // one context per search
+    const psg_config* c = configs[i];
+    total += c->n_entry_subset > 0 ? c->n_entry_subset
+                                   : plans[i]->n_plans * std::max(1, c->n_freqs);
+  }
+  std::vector<int> rc(size_t(n), PSG_OK);
+  auto run = [&](int i) {
+    ctxs[i]->concurrent_blocks = total;
+    rc[size_t(i)] = psg_search(ctxs[i], plans[i], clusters[i], stores[i], traces[i], configs[i], &outs[i]);
+    ctxs[i]->concurrent_blocks = 0;
+  };
+  std::vector<std::thread> pool;
+  for (int i = 1; i < n; ++i) pool.emplace_back(run, i);
+  run(0);
+  for (auto& t : pool) t.join();
+  for (int i = 0; i < n; ++i)
+    if (rc[size_t(i)] != PSG_OK) return rc[size_t(i)];
+  if (kernel_span_ms) {
+    // device span of the searches' kernels: earliest end of input H2D (ev[1])
+    // to the latest end of the reduction kernels (ev[3]), across streams
+    int first = 0;
+    for (int i = 1; i < n; ++i) {
+      float d = 0.f;
+      if (cudaEventElapsedTime(&d, ctxs[first]->ev[1], ctxs[i]->ev[1]) == cudaSuccess && d < 0.f) first = i;
+    }
+    double span = 0.0;
+    for (int i = 0; i < n; ++i) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, ctxs[first]->ev[1], ctxs[i]->ev[3]);
+      float extra = 0.f;  // compaction kernel of a detail search (ev[5] -> ev[6])
+      cudaEventElapsedTime(&extra, ctxs[i]->ev[5], ctxs[i]->ev[6]);
+      span = std::max(span, double(d) + double(extra));
+    }
+    *kernel_span_ms = span;
+  }
   return PSG_OK;
 }
 

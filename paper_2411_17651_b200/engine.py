@@ -147,8 +147,13 @@ class Engine:
         if rc != abi.PSG_OK:
             raise from_code(rc, f"psg_context_create(device={device}) failed (rc={rc})")
         self.handle = h
+        self.device = int(device)
+        self._extra = []
 
     def close(self):
+        for h in getattr(self, "_extra", []):
+            self.lib.psg_context_destroy(h)
+        self._extra = []
         if self.handle:
             self.lib.psg_context_destroy(self.handle)
             self.handle = None
@@ -172,6 +177,43 @@ class Engine:
             return SearchResult(out.contents, copy=copy, encodings=plans.encodings)
         finally:
             self.lib.psg_result_free(out)
+
+    def search_many(self, jobs, copy: bool = True) -> list:
+        """Several independent searches run concurrently on this device
+        (psg_search_many): jobs = [(plans, cluster, store, trace, config), ...].
+        Extra contexts (one per concurrent search) are created on demand;
+        .last_span_ms is the device time of the searches' kernels together."""
+        n = len(jobs)
+        if n == 0:
+            return []
+        while len(self._extra) < n - 1:
+            h = C.c_void_p()
+            rc = self.lib.psg_context_create(int(self.device), C.byref(h))
+            if rc != abi.PSG_OK:
+                raise from_code(rc, "psg_context_create failed")
+            self._extra.append(h)
+        handles = [self.handle] + self._extra[:n - 1]
+        cfgs = [j[4] or Config() for j in jobs]
+        arr = lambda items: (C.c_void_p * n)(*[C.addressof(x) for x in items])
+        ctxs = (C.c_void_p * n)(*[h.value for h in handles])
+        outs = (C.POINTER(abi.ResultC) * n)()
+        span = C.c_double(0.0)
+        rc = self.lib.psg_search_many(ctxs, n, arr([j[0].struct for j in jobs]),
+                                      arr([j[1].struct for j in jobs]), arr([j[2].struct for j in jobs]),
+                                      arr([j[3].struct for j in jobs]), arr([c.struct for c in cfgs]), outs,
+                                      C.byref(span))
+        self.last_span_ms = span.value
+        try:
+            if rc != abi.PSG_OK:
+                msg = next((self.lib.psg_last_error(h).decode() for h in handles
+                            if self.lib.psg_last_error(h)), "")
+                raise from_code(rc, msg)
+            return [SearchResult(outs[i].contents, copy=copy, encodings=jobs[i][0].encodings)
+                    for i in range(n)]
+        finally:
+            for i in range(n):
+                if outs[i]:
+                    self.lib.psg_result_free(outs[i])
 
     def rank_keys(self, keys: np.ndarray) -> np.ndarray:
         """Device ranking of gathered psg_rank_key records (multi-GPU merge)."""

@@ -1,0 +1,29 @@
+"""psg_search_many: several searches run concurrently on one device (one
+stream each) return exactly what the same searches return one at a time."""
+import pytest
+
+from harness import RefCase, compare_to_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def test_concurrent_searches_equal_sequential(engine, workdir):
+    cases = [RefCase(k, workdir) for k in ("c1", "c4", "c4e", "c3")]
+    jobs = [(c.plans, c.cluster, c.store, c.trace, c.config()) for c in cases]
+    many = engine.search_many(jobs)
+    assert engine.last_span_ms > 0
+    for c, res in zip(cases, many):
+        assert compare_to_ref(res, c.ref) == []
+        one = engine.search(c.plans, c.cluster, c.store, c.trace, c.config())
+        assert one.entries.tobytes() == res.entries.tobytes()
+        assert one.per_request.tobytes() == res.per_request.tobytes()
+        assert one.rejected_ids.tobytes() == res.rejected_ids.tobytes()
+
+
+def test_concurrent_search_error_reports_failing_search(engine, workdir):
+    from paper_2411_17651_b200.errors import UsageError
+    c = RefCase("c1", workdir)
+    bad = c.config(entry_subset=[10 ** 9])
+    with pytest.raises(UsageError):
+        engine.search_many([(c.plans, c.cluster, c.store, c.trace, c.config()),
+                            (c.plans, c.cluster, c.store, c.trace, bad)])
