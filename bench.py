@@ -201,7 +201,7 @@ def main():
         line = {"impl": "reference", "metric": "plan-iterations simulated/sec", "value": v,
                 "unit": "plan-iter/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-                "scaling": "strong",  # one fixed search per step, its entries sharded over the ranks "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": title, "design_spaces": keys},
                 "cpu_baseline": {"value": v, "unit": "plan-iter/s", "cores": jobs,
                                  "kind": "reference",
