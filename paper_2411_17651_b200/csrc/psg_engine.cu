@@ -126,6 +126,7 @@ struct psg_context {
   int n_sm = 148;                  // device properties used to size the simulation launch
   int64_t smem_sm = 228 * 1024, smem_block_max = 227 * 1024;
   int concurrent_blocks = 0;       // psg_search_many: simulation blocks sharing the device
+  int64_t sim_static_smem = 0;     // sim_kernel's static shared memory
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
@@ -180,7 +181,12 @@ int psg_context_create(int device, psg_context** out) {
   }
   // the cap only; each launch asks for what it needs (set once: contexts may
   // launch concurrently from several threads)
-  cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ctx->smem_block_max));
+  {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, sim_kernel) == cudaSuccess) ctx->sim_static_smem = int64_t(fa.sharedSizeBytes);
+  }
+  cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(ctx->smem_block_max - ctx->sim_static_smem));
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
   return PSG_OK;
@@ -643,6 +649,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.tab_smem = tab_smem;
   sp.chain_replicas = 1;
   if (const char* v = std::getenv("PSG_CHAIN_REPLICAS")) sp.chain_replicas = std::atoi(v) != 0;  // dev knob
+  sp.speculate = 1;
+  if (const char* v = std::getenv("PSG_SPECULATE")) sp.speculate = std::atoi(v) != 0;  // dev knob
   {
     // Active slots live in shared memory while they fit: give each unit as
     // many as keeps every unit resident in one wave (the kernel's time is its
@@ -652,7 +660,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     const int64_t want = std::max<int64_t>(256, (max_nr + 31) / 32 * 32);
     const int blocks = std::max(sp.chain_replicas ? E : n_units, ctx->concurrent_blocks);
     const int per_sm = std::max(1, (blocks + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
-    const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024);
+    const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024) -
+                           ctx->sim_static_smem;
     int64_t cap = 256;
     for (int64_t c = want; c > 256; c -= 32) {
       const int64_t l2 = (std::max<int64_t>(c, max_nr) + 1023) / 1024 + 1;
@@ -766,7 +775,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     ++launches;
   }
   if (n_units > 0) {
-    sim_kernel<<<sp.chain_replicas ? E : n_units, kWarp, smem, st>>>(sp);
+    sim_kernel<<<sp.chain_replicas ? E : n_units, sp.speculate ? 2 * kWarp : kWarp, smem, st>>>(sp);
     ++launches;
     PSG_CUDA(cudaGetLastError());
   }
@@ -798,7 +807,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
       sp.emit_jou = static_cast<double*>(ctx->d_ijou.p);
       sp.emit_off = static_cast<const int64_t*>(ctx->d_ioff.p);
       sp.emit_S = emit_S;
-      sim_kernel<<<sp.chain_replicas ? E : n_units, kWarp, smem, st>>>(sp);
+      sim_kernel<<<sp.chain_replicas ? E : n_units, sp.speculate ? 2 * kWarp : kWarp, smem, st>>>(sp);
       ++launches;
       PSG_CUDA(cudaGetLastError());
       // the stepwise pass is a replay: the first pass's outputs are rewritten bit-identically

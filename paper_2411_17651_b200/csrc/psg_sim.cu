@@ -47,7 +47,7 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 // Phase profiler (dev builds only: -DPSG_PHASE_PROFILE; zero code otherwise).
 // slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 decode cost,
 // 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
-// 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 -, 15 total.
+// 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 #speculation hits, 15 total.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -76,6 +76,19 @@ struct CurveDesc {
 
 __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+constexpr int kMemoCap = 256;  // decode-cost memo entries (SimParams::memo_cap must match)
+
+// Fixed-size per-unit state lives in static shared memory: constant addresses,
+// so the hot loops index it without recomputing a dynamic-shared base.
+__shared__ __align__(16) double s_qv[4 * kQvStride];              // query values (4 chains)
+__shared__ __align__(16) CurveDesc s_cdesc[kMaxClampSlots];       // staged curves
+__shared__ __align__(16) int64_t s_cellq[kMaxCells];              // qtab row 0 per cell
+__shared__ __align__(16) uint8_t s_p2p_slot[kMaxClampSlots];      // boundary -> distinct p2p curve
+__shared__ __align__(16) double s_p2p_val[2 * kMaxClampSlots];    // p2p (seconds, joules)
+__shared__ __align__(16) double s_w_arr[kWindow];                 // prefetch window: arrival
+__shared__ __align__(16) int32_t s_w_i32[4 * kWindow];            // tidx, ctx, gen, slot
+__shared__ __align__(16) double s_memo[4 * kMemoCap];             // decode-only cost per B
+
 struct SmemLayout {
   size_t qv, cdesc, cellq, p2p_slot, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
       cm1, cm2, tab, total;
@@ -84,14 +97,8 @@ struct SmemLayout {
 __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {
   SmemLayout L;
   size_t o = 0;
-  L.qv = o;        o = al16(o + sizeof(double) * 4 * kQvStride);
-  L.cdesc = o;     o = al16(o + sizeof(CurveDesc) * kMaxClampSlots);
-  L.cellq = o;     o = al16(o + sizeof(int64_t) * kMaxCells);
-  L.p2p_slot = o;  o = al16(o + kMaxClampSlots);
-  L.p2p_val = o;   o = al16(o + sizeof(double) * 2 * kMaxClampSlots);
-  L.win_arr = o;   o = al16(o + sizeof(double) * kWindow);
-  L.win_i32 = o;   o = al16(o + sizeof(int32_t) * 4 * kWindow);
-  L.memo = o;      o = al16(o + sizeof(double) * 4 * size_t(memo_cap));
+  (void)memo_cap;  // the fixed-size state is static shared memory (above)
+  L.qv = L.cdesc = L.cellq = L.p2p_slot = L.p2p_val = L.win_arr = L.win_i32 = L.memo = 0;
   L.act_f64 = o;   o = al16(o + sizeof(double) * 3 * size_t(smem_cap));
   L.act_fin = o;   o = al16(o + sizeof(int64_t) * size_t(smem_cap));
   L.act_i32 = o;   o = al16(o + sizeof(int32_t) * 6 * size_t(smem_cap));
@@ -100,6 +107,171 @@ __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_s
   L.tab = o;       o = al16(o + sizeof(double) * size_t(tab_smem));
   L.total = o;
   return L;
+}
+
+// Unit constants the cost evaluation reads (the main warp's registers; a
+// copy in shared memory for the speculation warp).
+struct EvalCtx {
+  const double* qtab;
+  uint64_t p2p_mask;
+  double sdd, reps, Sd;
+  int C, K, NQ, ND, NB, n_curve_knots;
+};
+
+struct EvalOut {
+  double cd, ce, cf, cb, srep, jrep;
+};
+
+// iteration_time (simulator.cpp:17-87) of {items, decode}: one lane per query
+// (cell lanes read their qtab row, curve lanes interpolate their staged
+// curve), lanes 0..3 run the four reference-ordered FP64 chains, then the
+// stage pass.  `item(i)` is the i-th prefill item's token count.  qv / p2p_val
+// are the calling warp's scratch.
+template <typename Item>
+__device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int lane, Item item,
+                                                  const int n_items, const int64_t decode,
+                                                  const int64_t total, const int64_t* cellq,
+                                                  CurveDesc* cdesc, const double* tab,
+                                                  const uint8_t* p2p_slot, double* qv,
+                                                  double* p2p_val) {
+  const int nq_c = n_items + (decode > 0 ? 1 : 0);
+  const int Qc = E.C * nq_c;
+  const int Q = Qc + E.NQ;
+  const double total_d = double(total);
+  // lanes 0..3 run the four reference-ordered chains (seconds, joules,
+  // flops, bytes); lanes 2, 3 stop at the cells (collectives add none)
+  double chain = 0.0;
+  const double* qrow = qv + (lane < 4 ? lane : 0) * kQvStride;
+  const float inv_nq = __frcp_rn(float(nq_c));
+  for (int base = 0; base < Q; base += kWarp) {
+    const int q = base + lane;
+    // cell query = one precomputed row {t, e_raw, flops, bytes}: issue the
+    // loads first so their latency overlaps the curve lanes' work
+    const bool cell_lane = q < Qc;
+    double2 te = make_double2(0.0, 0.0), fb = make_double2(0.0, 0.0);
+    if (cell_lane) {
+      const int c = int((float(q) + 0.5f) * inv_nq);  // q / nq_c (q, nq_c < 2^16)
+      const int i = q - c * nq_c;
+      const int64_t tok = i < n_items ? int64_t(item(i)) : decode;
+      const double2* row = reinterpret_cast<const double2*>(E.qtab + (cellq[c] + tok) * 4);
+      te = __ldg(row);
+      fb = __ldg(row + 1);
+    }
+    if (!cell_lane && q < Q) {
+      // collective / p2p curve query on the staged curve
+      const int k = q - Qc;
+      CurveDesc& d = cdesc[k];
+      const double x = __dmul_rn(__dmul_rn(d.ppt, total_d), d.share);
+      const double* kn = tab + d.kn_off;
+      const int cn = d.n;
+      // cnt = #knots <= x; the last interval usually still holds
+      const int h = d.hint;
+      int cnt;
+      if (h + 1 < cn && kn[h] <= x && x < kn[h + 1]) {
+        cnt = h + 1;
+      } else {
+        cnt = 0;
+        for (int j = 0; j < E.n_curve_knots; ++j)
+          cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
+        if (cnt >= 1 && cnt < cn) d.hint = cnt - 1;
+      }
+      const bool lo_c = x <= kn[0], hi_c = x >= kn[cn - 1];
+      const int lo = lo_c ? 0 : (hi_c ? cn - 1 : cnt - 1);
+      const int hi = lo_c ? 0 : (hi_c ? cn - 1 : cnt);
+      const bool interior = !(lo_c || hi_c);
+      const double t = __ddiv_rn(interior ? __dsub_rn(x, kn[lo]) : 0.0,
+                                 interior ? __dsub_rn(kn[hi], kn[lo]) : 1.0);
+      const double u = __dsub_rn(1.0, t);
+      const double* v = kn + cn;
+      const double sec = __dadd_rn(__dmul_rn(u, v[2 * lo]), __dmul_rn(t, v[2 * hi]));
+      const double jou = __dadd_rn(__dmul_rn(u, v[2 * lo + 1]), __dmul_rn(t, v[2 * hi + 1]));
+      const double en = __dmul_rn(jou, d.emul);
+      if (k >= E.K) {
+        p2p_val[k - E.K] = sec;
+        p2p_val[kMaxClampSlots + k - E.K] = en;
+      }
+      qv[lane] = sec;
+      qv[kQvStride + lane] = en;
+    }
+    if (cell_lane) {
+      qv[lane] = te.x;
+      qv[kQvStride + lane] = __dmul_rn(te.y, E.sdd);  // query_energy * stage_devices
+      qv[2 * kQvStride + lane] = fb.x;
+      qv[3 * kQvStride + lane] = fb.y;
+    }
+    __syncwarp();
+    const int here = min(kWarp, Q - base);
+    const int cell_end = min(here, max(0, Qc - base));
+    const int coll_end = min(here, max(0, Qc + E.K - base));
+    const int end = lane < 2 ? coll_end : (lane < 4 ? cell_end : 0);
+    int l = 0;
+    for (; l + 4 <= end; l += 4) {
+      const double v0 = qrow[l], v1 = qrow[l + 1], v2 = qrow[l + 2], v3 = qrow[l + 3];
+      chain = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(chain, v0), v1), v2), v3);
+    }
+    for (; l < end; ++l) chain = __dadd_rn(chain, qrow[l]);
+    __syncwarp();
+  }
+  const double bs = __shfl_sync(kFull, chain, 0);
+  const double bj = __shfl_sync(kFull, chain, 1);
+  const double bf = __shfl_sync(kFull, chain, 2);
+  const double bb = __shfl_sync(kFull, chain, 3);
+  // stages (simulator.cpp:64-78, :125-130): every stage prices the same
+  // block * reps; boundary b adds its p2p to stage b+1
+  EvalOut o;
+  o.srep = __dmul_rn(bs, E.reps);
+  o.jrep = __dmul_rn(bj, E.reps);
+  double cd = dmax_ref(0.0, o.srep);
+  double ce = __dadd_rn(0.0, o.jrep);
+  if (E.ND <= 2) {
+    const double s0 = __dadd_rn(o.srep, p2p_val[0]), s1 = __dadd_rn(o.srep, p2p_val[1]);
+    const double j0 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots]);
+    const double j1 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + 1]);
+    if (E.NB > 0) cd = dmax_ref(cd, s0);
+    if (E.ND == 2) cd = dmax_ref(cd, s1);
+    for (int b = 0; b < E.NB; ++b) ce = __dadd_rn(ce, ((E.p2p_mask >> b) & 1) ? j1 : j0);
+  } else {
+    for (int b = 0; b < E.NB; ++b) {
+      const int s = p2p_slot[b];
+      cd = dmax_ref(cd, __dadd_rn(o.srep, p2p_val[s]));
+      ce = __dadd_rn(ce, __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + s]));
+    }
+  }
+  o.cd = cd;
+  o.ce = ce;
+  o.cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, E.sdd), E.reps), E.Sd);
+  o.cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, E.sdd), E.reps), E.Sd);
+  return o;
+}
+
+// Speculative evaluation (block = 2 warps).  While the simulation warp runs a
+// decode run, the speculation warp prices the mixed iteration the queue head
+// will most likely trigger — items {head's first chunk}, decode = the current
+// batch — with the same eval_iteration; if the real iteration matches, the
+// simulation warp takes the result instead of pricing it.  Job hand-off is a
+// seqlock in shared memory (posted is odd while a job is being written).
+struct SpecSlot {
+  EvalCtx ctx;           // the running unit's constants (written while the helper is idle)
+  unsigned long long job;  // seq:20 | tok:22 | decode:22 — one store, no seqlock needed
+  int started;           // seq the helper is pricing
+  int done;              // seq of the results below
+  int quit;
+  int pad;
+  double cd, ce, cf, cb;
+};
+constexpr int kSpecField = 22;  // tok, decode < 2^22 to be speculated
+constexpr unsigned kSeqMask = (1u << 20) - 1u;
+__shared__ __align__(16) SpecSlot s_spec;
+__shared__ __align__(16) double s_qv2[4 * kQvStride];            // speculation warp scratch
+__shared__ __align__(16) double s_p2p_val2[2 * kMaxClampSlots];
+
+__device__ __forceinline__ int vload(const int& x) { return *reinterpret_cast<const volatile int*>(&x); }
+__device__ __forceinline__ void vstore(int& x, int v) { *reinterpret_cast<volatile int*>(&x) = v; }
+__device__ __forceinline__ unsigned long long vload64(const unsigned long long& x) {
+  return *reinterpret_cast<const volatile unsigned long long*>(&x);
+}
+__device__ __forceinline__ void vstore64(unsigned long long& x, unsigned long long v) {
+  *reinterpret_cast<volatile unsigned long long*>(&x) = v;
 }
 
 // max{T >= -1 : double(T) * kv <= cap} with the reference's exact product
@@ -131,14 +303,14 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
 #endif
 
   const SmemLayout L = smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap);
-  double* qv = reinterpret_cast<double*>(smem_raw + L.qv);
-  CurveDesc* cdesc = reinterpret_cast<CurveDesc*>(smem_raw + L.cdesc);
-  int64_t* cellq = reinterpret_cast<int64_t*>(smem_raw + L.cellq);  // qtab row 0 of each cell
-  uint8_t* p2p_slot = reinterpret_cast<uint8_t*>(smem_raw + L.p2p_slot);
-  double* p2p_val = reinterpret_cast<double*>(smem_raw + L.p2p_val);
-  double* w_arr = reinterpret_cast<double*>(smem_raw + L.win_arr);
-  int32_t* w_i32 = reinterpret_cast<int32_t*>(smem_raw + L.win_i32);  // tidx, ctx, gen, slot
-  double* memo = reinterpret_cast<double*>(smem_raw + L.memo);
+  double* qv = s_qv;
+  CurveDesc* cdesc = s_cdesc;
+  int64_t* cellq = s_cellq;
+  uint8_t* p2p_slot = s_p2p_slot;
+  double* p2p_val = s_p2p_val;
+  double* w_arr = s_w_arr;
+  int32_t* w_i32 = s_w_i32;
+  double* memo = s_memo;
   double* tab = reinterpret_cast<double*>(smem_raw + L.tab);
 
   // ---- plan constants (warp-uniform) ----
@@ -155,6 +327,13 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const int64_t cap_tok = ledger_cap_tokens(kv, cap);
   const double* qtab = p.qtab;
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
+
+  // the speculation warp reads the unit's staged state: let it go idle first
+  const bool spec_on = blockDim.x > kWarp && !p.emit_it;
+  if (spec_on)
+    while (unsigned(vload(s_spec.done)) != unsigned(vload64(s_spec.job) >> 44)) {
+    }
+  __syncwarp();
 
   // distinct p2p tables: boundaries only span 1 or 2 nodes in practice
   int ND = 0;
@@ -174,7 +353,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   uint64_t p2p_mask = 0;  // ND <= 2: bit b = distinct-curve slot of boundary b
   __syncwarp();
   for (int b = 0; b < NB && ND <= 2; ++b) p2p_mask |= uint64_t(p2p_slot[b]) << b;
-  for (int i = lane; i < 4 * p.memo_cap; i += kWarp) memo[i] = -1.0;
+  for (int i = lane; i < 4 * kMemoCap; i += kWarp) memo[i] = -1.0;
   if (lane < C) {
     const int sig = p.cell_sig[size_t(U.fslot) * p.n_cells_total + c0 + lane];
     cellq[lane] = p.qoff[sig];
@@ -218,6 +397,35 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   int n_curve_knots = 1;  // longest payload axis among the unit's curves
   for (int q = 0; q < NQ; ++q) n_curve_knots = max(n_curve_knots, cdesc[q].n);
   __syncwarp();
+  EvalCtx ectx;
+  ectx.qtab = qtab;
+  ectx.p2p_mask = p2p_mask;
+  ectx.sdd = sdd;
+  ectx.reps = reps;
+  ectx.Sd = Sd;
+  ectx.C = C;
+  ectx.K = K;
+  ectx.NQ = NQ;
+  ectx.ND = ND;
+  ectx.NB = NB;
+  ectx.n_curve_knots = n_curve_knots;
+  unsigned spec_seq = unsigned(vload64(s_spec.job) >> 44);  // last posted job (warp-uniform)
+  int spec_tok = -1;
+  int64_t spec_dec = -1;
+  if (spec_on && lane == 0) {
+    s_spec.ctx = ectx;
+    __threadfence_block();  // before any job of this unit
+  }
+  __syncwarp();
+  auto spec_post = [&](int tok, int64_t dec) {
+    spec_seq = (spec_seq + 1) & kSeqMask;
+    if (lane == 0)
+      vstore64(s_spec.job, (static_cast<unsigned long long>(spec_seq) << 44) |
+                               (static_cast<unsigned long long>(tok) << kSpecField) |
+                               static_cast<unsigned long long>(dec));
+    spec_tok = tok;
+    spec_dec = dec;
+  };
 
   // ---- active slots ----
   int cap_now = p.smem_cap;
@@ -540,111 +748,33 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
 
       // ---- iteration_time (simulator.cpp:17-87) ----
       PROF_T0(t_ev);
-      const int nq_c = n_items + (decode > 0 ? 1 : 0);
-      const int Qc = C * nq_c;
-      const int Q = Qc + NQ;
-      const double total_d = double(total);
-      // lanes 0..3 run the four reference-ordered chains (seconds, joules,
-      // flops, bytes); lanes 2, 3 stop at the cells (collectives add none)
-      double chain = 0.0;
-      const double* qrow = qv + (lane < 4 ? lane : 0) * kQvStride;
-      const float inv_nq = __frcp_rn(float(nq_c));
-      for (int base = 0; base < Q; base += kWarp) {
-        const int q = base + lane;
-        // cell query = one precomputed row {t, e_raw, flops, bytes}: issue the
-        // loads first so their latency overlaps the curve lanes' work
-        const bool cell_lane = q < Qc;
-        double2 te = make_double2(0.0, 0.0), fb = make_double2(0.0, 0.0);
-        if (cell_lane) {
-          const int c = int((float(q) + 0.5f) * inv_nq);  // q / nq_c (q, nq_c < 2^16)
-          const int i = q - c * nq_c;
-          const int64_t tok = i < n_items ? int64_t(a.items[i]) : decode;
-          const double2* row = reinterpret_cast<const double2*>(qtab + (cellq[c] + tok) * 4);
-          te = __ldg(row);
-          fb = __ldg(row + 1);
-        }
-        if (!cell_lane && q < Q) {
-          // collective / p2p curve query on the staged curve
-          const int k = q - Qc;
-          CurveDesc& d = cdesc[k];
-          const double x = __dmul_rn(__dmul_rn(d.ppt, total_d), d.share);
-          const double* kn = tab + d.kn_off;
-          const int cn = d.n;
-          // cnt = #knots <= x; the last interval usually still holds
-          const int h = d.hint;
-          int cnt;
-          if (h + 1 < cn && kn[h] <= x && x < kn[h + 1]) {
-            cnt = h + 1;
-          } else {
-            cnt = 0;
-            for (int j = 0; j < n_curve_knots; ++j)
-              cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
-            if (cnt >= 1 && cnt < cn) d.hint = cnt - 1;
-          }
-          const bool lo_c = x <= kn[0], hi_c = x >= kn[cn - 1];
-          const int lo = lo_c ? 0 : (hi_c ? cn - 1 : cnt - 1);
-          const int hi = lo_c ? 0 : (hi_c ? cn - 1 : cnt);
-          const bool interior = !(lo_c || hi_c);
-          const double t = __ddiv_rn(interior ? __dsub_rn(x, kn[lo]) : 0.0,
-                                     interior ? __dsub_rn(kn[hi], kn[lo]) : 1.0);
-          const double u = __dsub_rn(1.0, t);
-          const double* v = kn + cn;
-          const double sec = __dadd_rn(__dmul_rn(u, v[2 * lo]), __dmul_rn(t, v[2 * hi]));
-          const double jou = __dadd_rn(__dmul_rn(u, v[2 * lo + 1]), __dmul_rn(t, v[2 * hi + 1]));
-          const double en = __dmul_rn(jou, d.emul);
-          if (k >= K) {
-            p2p_val[k - K] = sec;
-            p2p_val[kMaxClampSlots + k - K] = en;
-          }
-          qv[lane] = sec;
-          qv[kQvStride + lane] = en;
-        }
-        if (cell_lane) {
-          qv[lane] = te.x;
-          qv[kQvStride + lane] = __dmul_rn(te.y, sdd);  // query_energy * stage_devices
-          qv[2 * kQvStride + lane] = fb.x;
-          qv[3 * kQvStride + lane] = fb.y;
-        }
-        __syncwarp();
-        PROF_ADD(14, t_ev);
-        const int here = min(kWarp, Q - base);
-        const int cell_end = min(here, max(0, Qc - base));
-        const int coll_end = min(here, max(0, Qc + K - base));
-        const int end = lane < 2 ? coll_end : (lane < 4 ? cell_end : 0);
-        int l = 0;
-        for (; l + 4 <= end; l += 4) {
-          const double v0 = qrow[l], v1 = qrow[l + 1], v2 = qrow[l + 2], v3 = qrow[l + 3];
-          chain = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(chain, v0), v1), v2), v3);
-        }
-        for (; l < end; ++l) chain = __dadd_rn(chain, qrow[l]);
-        __syncwarp();
+      EvalOut ev;
+      bool use_spec = false;
+      if (spec_on && n_items == 1 && decode == spec_dec && a.items[0] == spec_tok) {
+        // the speculation warp prices exactly this iteration: wait for it if
+        // it has started (it is ahead of us), else price it here
+        const unsigned st = unsigned(__shfl_sync(kFull, vload(s_spec.started), 0));
+        use_spec = st == spec_seq;
       }
-      const double bs = __shfl_sync(kFull, chain, 0);
-      const double bj = __shfl_sync(kFull, chain, 1);
-      const double bf = __shfl_sync(kFull, chain, 2);
-      const double bb = __shfl_sync(kFull, chain, 3);
-      // stages (simulator.cpp:64-78, :125-130): every stage prices the same
-      // block * reps; boundary b adds its p2p to stage b+1
-      const double srep = __dmul_rn(bs, reps);
-      const double jrep = __dmul_rn(bj, reps);
-      double cd = dmax_ref(0.0, srep);
-      double ce = __dadd_rn(0.0, jrep);
-      if (ND <= 2) {
-        const double s0 = __dadd_rn(srep, p2p_val[0]), s1 = __dadd_rn(srep, p2p_val[1]);
-        const double j0 = __dadd_rn(jrep, p2p_val[kMaxClampSlots]);
-        const double j1 = __dadd_rn(jrep, p2p_val[kMaxClampSlots + 1]);
-        if (NB > 0) cd = dmax_ref(cd, s0);
-        if (ND == 2) cd = dmax_ref(cd, s1);
-        for (int b = 0; b < NB; ++b) ce = __dadd_rn(ce, ((p2p_mask >> b) & 1) ? j1 : j0);
+      if (use_spec) {
+        PROF_CNT(14);
+        while (unsigned(vload(s_spec.done)) != spec_seq) {
+        }
+        __threadfence_block();
+        ev.cd = s_spec.cd;
+        ev.ce = s_spec.ce;
+        ev.cf = s_spec.cf;
+        ev.cb = s_spec.cb;
+        ev.srep = ev.jrep = 0.0;  // stage values only matter when emitting (no speculation)
+        spec_tok = -1;
+        __syncwarp();
       } else {
-        for (int b = 0; b < NB; ++b) {
-          const int s = p2p_slot[b];
-          cd = dmax_ref(cd, __dadd_rn(srep, p2p_val[s]));
-          ce = __dadd_rn(ce, __dadd_rn(jrep, p2p_val[kMaxClampSlots + s]));
-        }
+        ev = eval_iteration(
+            ectx, lane, [&](int i) { return a.items[i]; }, n_items, decode, total, cellq, cdesc,
+            tab, p2p_slot, qv, p2p_val);
       }
-      const double cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
-      const double cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
+      const double srep = ev.srep, jrep = ev.jrep;
+      const double cd = ev.cd, ce = ev.ce, cf = ev.cf, cb = ev.cb;
       if (stepwise) {  // IterationRecord (simulator.cpp:158-170)
         const int64_t r = p.emit_off[unit_idx] + n;
         if (lane == 0) {
@@ -726,7 +856,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       PROF_CNT(11);
       PROF_T0(t_d1);
       double d, e, f, b;
-      if (B <= p.memo_cap && memo[4 * (B - 1)] >= 0.0) {
+      if (B <= kMemoCap && memo[4 * (B - 1)] >= 0.0) {
         d = memo[4 * (B - 1)];
         e = memo[4 * (B - 1) + 1];
         f = memo[4 * (B - 1) + 2];
@@ -739,7 +869,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         e = de.y;
         f = fb.x;
         b = fb.y;
-        if (B <= p.memo_cap) {
+        if (B <= kMemoCap) {
           if (lane == 0) {
             memo[4 * (B - 1) + 1] = e;
             memo[4 * (B - 1) + 2] = f;
@@ -768,6 +898,17 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         } else if (!(max_bs > 0 && int64_t(B) >= max_bs) && used + hd_ctx <= cap_tok) {
           check = true;  // admissible at iteration start j while used + j*B + ctx fits
         }
+      }
+      // speculate only when the head arrives before the next finish (the batch
+      // it joins is then exactly this one); the estimate only picks jobs,
+      // correctness comes from the exact match at use
+      if (spec_on && n_pre == 0 && hd_valid && !hd_stack && hd_arr > clock && !rej_h &&
+          hd_arr < clock + double(next_fin - n) * d) {
+        int64_t first = hd_ctx;  // the head's first prefill chunk
+        if (chunked && first > chunk) first = chunk;
+        if ((int(first) != spec_tok || int64_t(B) != spec_dec) && first < (1 << kSpecField) &&
+            B < (1 << kSpecField))
+          spec_post(int(first), int64_t(B));
       }
       bool stop = false;
       PROF_ADD(5, t_d2);
@@ -1013,20 +1154,66 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   }
 }
 
-__global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double tf = 0.0, tb = 0.0;
-  if (p.chain_replicas) {
-    // one warp per entry: its replicas in order, one running tally — the
-    // reference's WorkTally, so MFU / MBU are bit-exact for DP > 1
-    const int e = blockIdx.x;
-    for (int k = p.entry_unit_begin[e]; k < p.entry_unit_begin[e + 1]; ++k) {
-      sim_unit(p, p.entry_units[k], tf, tb, smem_raw);
-      __syncwarp();
+// The speculation warp: prices posted jobs until the simulation warp quits.
+__device__ __noinline__ void spec_helper(const double* tab) {
+  const int lane = threadIdx.x - kWarp;
+  unsigned last = 0;
+  while (true) {
+    unsigned long long job;
+    while (true) {
+      job = __shfl_sync(kFull, vload64(s_spec.job), 0);
+      if (unsigned(job >> 44) != last) break;
+      if (__shfl_sync(kFull, vload(s_spec.quit), 0)) return;
+      __nanosleep(20);
     }
-  } else {
-    sim_unit(p, blockIdx.x, tf, tb, smem_raw);
+    const unsigned sq = unsigned(job >> 44);
+    const int tok = int((job >> kSpecField) & ((1ull << kSpecField) - 1));
+    const int64_t dec = int64_t(job & ((1ull << kSpecField) - 1));
+    if (lane == 0) vstore(s_spec.started, int(sq));
+    __threadfence_block();
+    const EvalCtx E = s_spec.ctx;
+    const EvalOut o = eval_iteration(
+        E, lane, [&](int) { return tok; }, 1, dec, dec + tok, s_cellq, s_cdesc, tab, s_p2p_slot,
+        s_qv2, s_p2p_val2);
+    if (lane == 0) {
+      s_spec.cd = o.cd;
+      s_spec.ce = o.ce;
+      s_spec.cf = o.cf;
+      s_spec.cb = o.cb;
+      __threadfence_block();
+      vstore(s_spec.done, int(sq));
+    }
+    __syncwarp();
+    last = sq;
   }
+}
+
+__global__ void __launch_bounds__(64, 4) sim_kernel(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (threadIdx.x == 0) {
+    s_spec.job = 0;
+    s_spec.started = 0;
+    s_spec.done = 0;
+    s_spec.quit = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= kWarp) {  // blockDim 64: the speculation warp
+    spec_helper(reinterpret_cast<const double*>(
+        smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab));
+    return;
+  }
+  double tf = 0.0, tb = 0.0;
+  // chained: one warp per entry runs its replicas in order with one running
+  // tally (the reference's WorkTally, so MFU / MBU are bit-exact for DP > 1);
+  // else one warp per unit.  One call site keeps one copy of the loop's code.
+  const int e = blockIdx.x;
+  const int k0 = p.chain_replicas ? p.entry_unit_begin[e] : e;
+  const int k1 = p.chain_replicas ? p.entry_unit_begin[e + 1] : e + 1;
+  for (int k = k0; k < k1; ++k) {
+    sim_unit(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) vstore(s_spec.quit, 1);
 }
 
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {

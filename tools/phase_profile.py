@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.join(REPO, "oracle"))
 sys.path.insert(0, os.path.join(REPO, "tests"))
 
 NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
-         "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "eval_part1", "total"]
+         "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total"]
 
 
 def main():
@@ -53,8 +53,8 @@ def run(key, args):
     for u in order[:args.top]:
         tot = float(cnt[u, 15])
         enc = case.plans.encodings[int(meta[u, 0]) // F]
-        parts = " ".join(f"{NAMES[k]}={100 * cnt[u, k] / tot:.1f}%" for k in list(range(10)) + [14])
-        counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 14))
+        parts = " ".join(f"{NAMES[k]}={100 * cnt[u, k] / tot:.1f}%" for k in range(10))
+        counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 15))
         print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
 
 
