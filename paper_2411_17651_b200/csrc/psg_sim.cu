@@ -329,7 +329,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
 
   // the speculation warp reads the unit's staged state: let it go idle first
-  const bool spec_on = blockDim.x > kWarp && !p.emit_it;
+  const bool spec_on = blockDim.x > kWarp && !p.emit_it && p.speculate == 1;  // 2: helper idles (dev)
   if (spec_on)
     while (unsigned(vload(s_spec.done)) != unsigned(vload64(s_spec.job) >> 44)) {
     }
