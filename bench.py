@@ -358,7 +358,7 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "psg::sim_kernel",
+                     "kernel": prof.get("kernel", "psg::sim_kernel_spec"),
                      "algorithmic_bytes_per_launch": alg_bytes / (len(steps) * sims_per_step),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "issue_slots_busy_pct": prof.get("issue_slots_busy_pct"),

@@ -140,6 +140,13 @@ struct psg_context {
 
 namespace {
 
+void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
+  if (sp.speculate)
+    sim_kernel_spec<<<blocks, 2 * kWarp, smem, st>>>(sp);
+  else
+    sim_kernel<<<blocks, kWarp, smem, st>>>(sp);
+}
+
 int fail(psg_context* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
@@ -181,12 +188,14 @@ int psg_context_create(int device, psg_context** out) {
   }
   // the cap only; each launch asks for what it needs (set once: contexts may
   // launch concurrently from several threads)
-  {
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec}) {
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, sim_kernel) == cudaSuccess) ctx->sim_static_smem = int64_t(fa.sharedSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k) == cudaSuccess)
+      ctx->sim_static_smem = std::max<int64_t>(ctx->sim_static_smem, int64_t(fa.sharedSizeBytes));
   }
-  cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(ctx->smem_block_max - ctx->sim_static_smem));
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(ctx->smem_block_max - ctx->sim_static_smem));
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
   return PSG_OK;
@@ -775,7 +784,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     ++launches;
   }
   if (n_units > 0) {
-    sim_kernel<<<sp.chain_replicas ? E : n_units, sp.speculate ? 2 * kWarp : kWarp, smem, st>>>(sp);
+    launch_sim(sp.chain_replicas ? E : n_units, smem, st, sp);
     ++launches;
     PSG_CUDA(cudaGetLastError());
   }
@@ -807,7 +816,7 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
       sp.emit_jou = static_cast<double*>(ctx->d_ijou.p);
       sp.emit_off = static_cast<const int64_t*>(ctx->d_ioff.p);
       sp.emit_S = emit_S;
-      sim_kernel<<<sp.chain_replicas ? E : n_units, sp.speculate ? 2 * kWarp : kWarp, smem, st>>>(sp);
+      launch_sim(sp.chain_replicas ? E : n_units, smem, st, sp);
       ++launches;
       PSG_CUDA(cudaGetLastError());
       // the stepwise pass is a replay: the first pass's outputs are rewritten bit-identically

@@ -39,7 +39,8 @@ struct ReduceParams {
   psg_rank_key* keys;
 };
 
-__global__ void sim_kernel(const SimParams p);
+__global__ void sim_kernel(const SimParams p);       // one warp per block
+__global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per block
 __global__ void entry_reduce_kernel(const ReduceParams r);
 __global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
                                int64_t* rj_off, int64_t* totals);

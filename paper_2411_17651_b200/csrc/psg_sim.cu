@@ -291,6 +291,7 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 
 // One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
 // carry WorkTally across the entry's replicas (simulator.cpp:195-201).
+template <bool kSpec>
 __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
                                          double& tally_flops, double& tally_bytes,
                                          unsigned char* smem_raw) {
@@ -329,7 +330,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
 
   // the speculation warp reads the unit's staged state: let it go idle first
-  const bool spec_on = blockDim.x > kWarp && !p.emit_it && p.speculate == 1;  // 2: helper idles (dev)
+  const bool spec_on = kSpec && !p.emit_it && p.speculate == 1;  // 2: helper idles (dev)
   if (spec_on)
     while (unsigned(vload(s_spec.done)) != unsigned(vload64(s_spec.job) >> 44)) {
     }
@@ -1188,20 +1189,9 @@ __device__ __noinline__ void spec_helper(const double* tab) {
   }
 }
 
-__global__ void __launch_bounds__(64, 4) sim_kernel(const SimParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (threadIdx.x == 0) {
-    s_spec.job = 0;
-    s_spec.started = 0;
-    s_spec.done = 0;
-    s_spec.quit = 0;
-  }
-  __syncthreads();
-  if (threadIdx.x >= kWarp) {  // blockDim 64: the speculation warp
-    spec_helper(reinterpret_cast<const double*>(
-        smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab));
-    return;
-  }
+// One warp per entry (or unit); with kSpec a second warp per block speculates.
+template <bool kSpec>
+__device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
   double tf = 0.0, tb = 0.0;
   // chained: one warp per entry runs its replicas in order with one running
   // tally (the reference's WorkTally, so MFU / MBU are bit-exact for DP > 1);
@@ -1210,10 +1200,32 @@ __global__ void __launch_bounds__(64, 4) sim_kernel(const SimParams p) {
   const int k0 = p.chain_replicas ? p.entry_unit_begin[e] : e;
   const int k1 = p.chain_replicas ? p.entry_unit_begin[e + 1] : e + 1;
   for (int k = k0; k < k1; ++k) {
-    sim_unit(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
+    sim_unit<kSpec>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (threadIdx.x == 0) {
+    s_spec.job = 0;
+    s_spec.started = 0;
+    s_spec.done = 0;
+    s_spec.quit = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= kWarp) {  // the speculation warp
+    spec_helper(reinterpret_cast<const double*>(
+        smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab));
+    return;
+  }
+  sim_block<true>(p, smem_raw);
   if (threadIdx.x == 0) vstore(s_spec.quit, 1);
+}
+
+__global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sim_block<false>(p, smem_raw);
 }
 
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {

@@ -48,3 +48,22 @@ def test_c2_matches_reference(engine, workdir, key):
     res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
     bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
     assert not bad, "\n".join(bad)
+
+
+KERNEL_MODES = [("0", "1"), ("1", "1"), ("0", "0"), ("1", "0")]  # (PSG_SPECULATE, PSG_CHAIN_REPLICAS)
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("spec,chain", KERNEL_MODES, ids=[f"spec{s}-chain{c}" for s, c in KERNEL_MODES])
+@pytest.mark.parametrize("key", ["c1", "c4"])
+def test_kernel_variants_match_reference(engine, workdir, monkeypatch, key, spec, chain):
+    """Both simulation kernels (with / without the speculation warp) and both
+    replica modes (chained tally / one warp per replica) give the reference's
+    results; unchained, MFU/MBU of DP>1 entries are per-replica partial sums
+    (within 1e-9)."""
+    monkeypatch.setenv("PSG_SPECULATE", spec)
+    monkeypatch.setenv("PSG_CHAIN_REPLICAS", chain)
+    case = RefCase(key, workdir)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0 if chain == "1" else 1e-9)
+    assert not bad, "\n".join(bad)
