@@ -254,6 +254,11 @@ struct GridSpec {
 };
 
 ProfileStore synth_profiles(const DeviceSpec& hw, const ClusterSpec& net, const GridSpec& grid);
+class Engine;
+// The same store with the compute tables computed on the GPU (psg_synth_compute;
+// SURVEY.md §8(f) row 4); byte-identical to synth_profiles.
+ProfileStore synth_profiles_device(const DeviceSpec& hw, const ClusterSpec& net,
+                                   const GridSpec& grid, Engine* engine = nullptr);
 
 // ---- traces (traces.hpp) -------------------------------------------------------
 struct Request {

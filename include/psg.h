@@ -264,6 +264,22 @@ typedef struct psg_result {
   double* stage_joules;               /* [n_iterations][n_stages] */
 } psg_result;
 
+/* Device synthesis of the analytical roofline compute tables (synth_profiles,
+   cost.cpp:454-487): values for every (variant, op, ctx, tasks, width) in the
+   reference's loop order, variant = (dtype, frequency) in loop order, op in
+   {attention, gemm, moe_gemm}. */
+typedef struct psg_synth_grid {
+  int32_t n_ctx, n_tasks, n_width, n_variants;
+  const double* ctx;                  /* GridSpec::context_knots */
+  const double* tasks;                /* GridSpec::task_knots */
+  const double* width;                /* GridSpec::width_knots */
+  const double* peak_scaled;          /* per variant: peak_flops_for(dtype) * (f / f_max) */
+  const double* elem_bytes;           /* per variant: 2 (fp16), 1 (fp8), 0.5 */
+  const double* power;                /* per variant: tdp * scale * scale * scale */
+  double mem_bw;                      /* DeviceSpec::peak_mem_bandwidth */
+  double hidden, head_dim, kv_elems;  /* GridSpec::shape */
+} psg_synth_grid;
+
 typedef struct psg_context psg_context;
 
 const char* psg_version(void);
@@ -272,6 +288,10 @@ const char* psg_version(void);
 int psg_context_create(int device, psg_context** out);
 void psg_context_destroy(psg_context* ctx);
 const char* psg_last_error(const psg_context* ctx);
+
+/* seconds / joules: n_variants * 3 * n_ctx * n_tasks * n_width values each. */
+int psg_synth_compute(psg_context* ctx, const psg_synth_grid* grid, double* seconds,
+                      double* joules);
 
 /* Evaluate-all-plans: plansim::search semantics (see header comment). */
 int psg_search(psg_context* ctx, const psg_plan_set* plans,

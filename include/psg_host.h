@@ -39,6 +39,8 @@ int psgh_problem_create(const char* model_json, const char* cluster_json,
 void psgh_problem_destroy(psgh_problem* p);
 
 int psgh_store_synth(psgh_problem* p, double max_context);
+/* synth_profiles with the compute tables computed on the GPU (device 0). */
+int psgh_store_synth_device(psgh_problem* p, double max_context);
 int psgh_store_load(psgh_problem* p, const char* jsonl);
 int psgh_trace_synth(psgh_problem* p, double ctx_mean, double ctx_std, double gen_mean,
                      double gen_std, double rate, int64_t n, uint64_t seed);

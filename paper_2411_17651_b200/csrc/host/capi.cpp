@@ -106,6 +106,13 @@ int psgh_store_synth(psgh_problem* p, double max_context) {
   });
 }
 
+int psgh_store_synth_device(psgh_problem* p, double max_context) {
+  return guarded([&] {
+    p->store = psb::synth_profiles_device(p->cluster.device, p->cluster,
+                                          psb::GridSpec::for_model(p->model, p->cluster, max_context));
+  });
+}
+
 int psgh_store_load(psgh_problem* p, const char* jsonl) {
   return guarded([&] { p->store = psb::ProfileStore::load(jsonl ? jsonl : ""); });
 }

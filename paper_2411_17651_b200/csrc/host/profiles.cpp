@@ -4,6 +4,7 @@
 // byte-compared with the reference's in tests/test_host_inputs.py.
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <set>
 #include <sstream>
 
@@ -269,25 +270,11 @@ GridSpec GridSpec::for_model(const ModelSpec& model, const ClusterSpec& cluster,
   return g;
 }
 
-ProfileStore synth_profiles(const DeviceSpec& hw, const ClusterSpec& net, const GridSpec& grid) {
-  ProfileStore store;
-  const double f_max = hw.max_frequency();
-  for (const Dtype dt : grid.dtypes) {
-    const double peak = hw.peak_flops_for(dt);
-    const double eb = dt == Dtype::FP16 ? 2.0 : dt == Dtype::FP8 ? 1.0 : 0.5;
-    for (const double f : hw.frequency_options) {
-      const double scale = f / f_max;
-      const double power = hw.tdp_watts * scale * scale * scale;  // cube-law DVFS power
-      for (const OpKind op : {OpKind::Attention, OpKind::GEMM, OpKind::MoEGEMM})
-        for (const double t : grid.context_knots)
-          for (const double k : grid.task_knots)
-            for (const double w : grid.width_knots) {
-              const double sec = std::max(op_flops(op, t, k, w, grid.shape) / (peak * scale),
-                                          op_bytes(op, t, k, w, grid.shape, eb) / hw.peak_mem_bandwidth);
-              store.add_compute_entry(op, dt, f, t, k, w, sec, sec * power);
-            }
-    }
-  }
+namespace {
+
+// The alpha-beta collective curves of synth_profiles (cost.cpp:489-506).
+void add_synth_collectives(ProfileStore& store, const DeviceSpec& hw, const ClusterSpec& net,
+                           const GridSpec& grid) {
   for (const auto& [devices, nodes] : grid.collective_groups) {
     int level = 1;  // the link level a group spanning `nodes` nodes must cross
     if (nodes > 1) {
@@ -315,6 +302,89 @@ ProfileStore synth_profiles(const DeviceSpec& hw, const ClusterSpec& net, const 
       }
     }
   }
+}
+
+constexpr OpKind kSynthOps[3] = {OpKind::Attention, OpKind::GEMM, OpKind::MoEGEMM};
+
+}  // namespace
+
+ProfileStore synth_profiles(const DeviceSpec& hw, const ClusterSpec& net, const GridSpec& grid) {
+  ProfileStore store;
+  const double f_max = hw.max_frequency();
+  for (const Dtype dt : grid.dtypes) {
+    const double peak = hw.peak_flops_for(dt);
+    const double eb = dt == Dtype::FP16 ? 2.0 : dt == Dtype::FP8 ? 1.0 : 0.5;
+    for (const double f : hw.frequency_options) {
+      const double scale = f / f_max;
+      const double power = hw.tdp_watts * scale * scale * scale;  // cube-law DVFS power
+      for (const OpKind op : kSynthOps)
+        for (const double t : grid.context_knots)
+          for (const double k : grid.task_knots)
+            for (const double w : grid.width_knots) {
+              const double sec = std::max(op_flops(op, t, k, w, grid.shape) / (peak * scale),
+                                          op_bytes(op, t, k, w, grid.shape, eb) / hw.peak_mem_bandwidth);
+              store.add_compute_entry(op, dt, f, t, k, w, sec, sec * power);
+            }
+    }
+  }
+  add_synth_collectives(store, hw, net, grid);
+  store.finalize();
+  return store;
+}
+
+ProfileStore synth_profiles_device(const DeviceSpec& hw, const ClusterSpec& net,
+                                   const GridSpec& grid, Engine* engine) {
+  std::unique_ptr<Engine> own;
+  if (!engine) {
+    own = std::make_unique<Engine>(0);
+    engine = own.get();
+  }
+  const double f_max = hw.max_frequency();
+  std::vector<double> peak_scaled, elem_bytes, power;
+  for (const Dtype dt : grid.dtypes) {
+    const double peak = hw.peak_flops_for(dt);
+    const double eb = dt == Dtype::FP16 ? 2.0 : dt == Dtype::FP8 ? 1.0 : 0.5;
+    for (const double f : hw.frequency_options) {
+      const double scale = f / f_max;
+      peak_scaled.push_back(peak * scale);
+      elem_bytes.push_back(eb);
+      power.push_back(hw.tdp_watts * scale * scale * scale);
+    }
+  }
+  psg_synth_grid g{};
+  g.n_ctx = int32_t(grid.context_knots.size());
+  g.n_tasks = int32_t(grid.task_knots.size());
+  g.n_width = int32_t(grid.width_knots.size());
+  g.n_variants = int32_t(peak_scaled.size());
+  g.ctx = grid.context_knots.data();
+  g.tasks = grid.task_knots.data();
+  g.width = grid.width_knots.data();
+  g.peak_scaled = peak_scaled.data();
+  g.elem_bytes = elem_bytes.data();
+  g.power = power.data();
+  g.mem_bw = hw.peak_mem_bandwidth;
+  g.hidden = grid.shape.model_hidden;
+  g.head_dim = grid.shape.head_dim;
+  g.kv_elems = grid.shape.kv_elems_per_task_token;
+  const size_t n = size_t(g.n_variants) * 3 * grid.context_knots.size() * grid.task_knots.size() *
+                   grid.width_knots.size();
+  std::vector<double> sec(n), jou(n);
+  ProfileStore store;
+  if (n > 0) {
+    const int rc = psg_synth_compute(engine->handle(), &g, sec.data(), jou.data());
+    if (rc != PSG_OK) throw DataError(std::string("synth on device: ") + psg_last_error(engine->handle()));
+  }
+  size_t i = 0;  // the values are in the reference's loop order
+  for (const Dtype dt : grid.dtypes)
+    for (const double f : hw.frequency_options)
+      for (const OpKind op : kSynthOps)
+        for (const double t : grid.context_knots)
+          for (const double k : grid.task_knots)
+            for (const double w : grid.width_knots) {
+              store.add_compute_entry(op, dt, f, t, k, w, sec[i], jou[i]);
+              ++i;
+            }
+  add_synth_collectives(store, hw, net, grid);
   store.finalize();
   return store;
 }

@@ -132,7 +132,7 @@ struct psg_context {
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
-  DevBuf d_it, d_isec, d_ijou, d_ioff;
+  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
   std::vector<uint8_t> compute_clamp, curve_clamp;
@@ -160,6 +160,47 @@ int fail(psg_context* ctx, int code, const std::string& msg) {
   } while (0)
 
 }  // namespace
+
+namespace psg {
+
+int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, double* joules) {
+  if (!ctx || !g || !seconds || !joules) return PSG_ERR_USAGE;
+  if (g->n_ctx < 1 || g->n_tasks < 1 || g->n_width < 1 || g->n_variants < 0)
+    return fail(ctx, PSG_ERR_USAGE, "synth: empty grid axis");
+  const int64_t total = int64_t(g->n_variants) * 3 * g->n_ctx * g->n_tasks * g->n_width;
+  if (total == 0) return PSG_OK;
+  PSG_CUDA(cudaSetDevice(ctx->device));
+  Packer pk;
+  const size_t oc = pk.add(g->ctx, size_t(g->n_ctx)), ot = pk.add(g->tasks, size_t(g->n_tasks)),
+               ow = pk.add(g->width, size_t(g->n_width)),
+               op = pk.add(g->peak_scaled, size_t(g->n_variants)),
+               oe = pk.add(g->elem_bytes, size_t(g->n_variants)),
+               ob = pk.add(g->power, size_t(g->n_variants));
+  const size_t in_bytes = (pk.size + 15) & ~size_t(15);
+  PSG_CUDA(ctx->d_synth.ensure(in_bytes + 2 * size_t(total) * sizeof(double)));
+  PSG_CUDA(ctx->h_in.ensure(in_bytes));
+  pk.write(static_cast<unsigned char*>(ctx->h_in.p));
+  auto* d = static_cast<unsigned char*>(ctx->d_synth.p);
+  PSG_CUDA(cudaMemcpyAsync(d, ctx->h_in.p, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  psg_synth_grid dg = *g;
+  dg.ctx = reinterpret_cast<const double*>(d + oc);
+  dg.tasks = reinterpret_cast<const double*>(d + ot);
+  dg.width = reinterpret_cast<const double*>(d + ow);
+  dg.peak_scaled = reinterpret_cast<const double*>(d + op);
+  dg.elem_bytes = reinterpret_cast<const double*>(d + oe);
+  dg.power = reinterpret_cast<const double*>(d + ob);
+  double* dsec = reinterpret_cast<double*>(d + in_bytes);
+  double* djou = dsec + total;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, int64_t(ctx->n_sm) * 8);
+  synth_compute_kernel<<<unsigned(blocks), 256, 0, ctx->stream>>>(dg, dsec, djou);
+  PSG_CUDA(cudaGetLastError());
+  PSG_CUDA(cudaMemcpyAsync(seconds, dsec, size_t(total) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaMemcpyAsync(joules, djou, size_t(total) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PSG_OK;
+}
+
+}  // namespace psg
 
 extern "C" {
 
@@ -207,7 +248,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
                     &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
-                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff})
+                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj, &ctx->h_it, &ctx->h_isec, &ctx->h_ijou})
     b->release();

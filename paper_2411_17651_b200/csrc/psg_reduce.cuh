@@ -39,6 +39,8 @@ struct ReduceParams {
   psg_rank_key* keys;
 };
 
+__global__ void synth_compute_kernel(const psg_synth_grid g, double* sec, double* jou);
+int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, double* joules);
 __global__ void sim_kernel(const SimParams p);       // one warp per block
 __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per block
 __global__ void entry_reduce_kernel(const ReduceParams r);

@@ -33,6 +33,7 @@ def _lib():
                                         C.POINTER(v)]
     lib.psgh_problem_destroy.argtypes = [v]
     lib.psgh_store_synth.argtypes = [v, C.c_double]
+    lib.psgh_store_synth_device.argtypes = [v, C.c_double]
     lib.psgh_store_load.argtypes = [v, C.c_char_p]
     lib.psgh_trace_synth.argtypes = [v, C.c_double, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int64, C.c_uint64]
@@ -96,8 +97,11 @@ class Problem:
             pass
 
     # ---- inputs ----
-    def synth_store(self, max_context=131072.0):
-        self._check(self.lib.psgh_store_synth(self.h, float(max_context)))
+    def synth_store(self, max_context=131072.0, device=False):
+        """synth_profiles (cost.cpp:454-509); device=True computes the compute
+        tables on the GPU (byte-identical store)."""
+        fn = self.lib.psgh_store_synth_device if device else self.lib.psgh_store_synth
+        self._check(fn(self.h, float(max_context)))
         return self
 
     def load_store(self, jsonl: str):
