@@ -93,6 +93,7 @@ struct SimParams {
   int32_t serial_run;        // decode-run iterations stepped serially before the closed form
   int32_t chain_replicas;    // 1: grid = entries, replicas run in order with one tally
   int32_t speculate;         // 1: blockDim 64, a second warp prices the next mixed iteration
+  int32_t spec_sleep_ns;     // the speculation warp's polling interval
   const int32_t* entry_unit_begin;  // [E+1] units of entry e (replica order) ...
   const int32_t* entry_units;       // ... as unit indices
   int32_t tab_smem;          // doubles of per-unit curve staging in shared memory

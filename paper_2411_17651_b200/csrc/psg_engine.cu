@@ -701,6 +701,8 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   if (const char* v = std::getenv("PSG_CHAIN_REPLICAS")) sp.chain_replicas = std::atoi(v) != 0;  // dev knob
   sp.speculate = 1;
   if (const char* v = std::getenv("PSG_SPECULATE")) sp.speculate = std::atoi(v);  // dev knob: 0 off, 2 idle helper
+  sp.spec_sleep_ns = 20;
+  if (const char* v = std::getenv("PSG_SPEC_SLEEP_NS")) sp.spec_sleep_ns = std::max(0, std::atoi(v));  // dev knob
   {
     // Active slots live in shared memory while they fit: give each unit as
     // many as keeps every unit resident in one wave (the kernel's time is its

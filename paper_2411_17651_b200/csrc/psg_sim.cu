@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
 }
 
 // The speculation warp: prices posted jobs until the simulation warp quits.
-__device__ __noinline__ void spec_helper(const double* tab) {
+__device__ __noinline__ void spec_helper(const double* tab, const unsigned sleep_ns) {
   const int lane = threadIdx.x - kWarp;
   unsigned last = 0;
   while (true) {
@@ -1165,7 +1165,7 @@ __device__ __noinline__ void spec_helper(const double* tab) {
       job = __shfl_sync(kFull, vload64(s_spec.job), 0);
       if (unsigned(job >> 44) != last) break;
       if (__shfl_sync(kFull, vload(s_spec.quit), 0)) return;
-      __nanosleep(20);
+      __nanosleep(sleep_ns);
     }
     const unsigned sq = unsigned(job >> 44);
     const int tok = int((job >> kSpecField) & ((1ull << kSpecField) - 1));
@@ -1216,7 +1216,8 @@ __global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) {
   __syncthreads();
   if (threadIdx.x >= kWarp) {  // the speculation warp
     spec_helper(reinterpret_cast<const double*>(
-        smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab));
+                    smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab),
+                unsigned(p.spec_sleep_ns));
     return;
   }
   sim_block<true>(p, smem_raw);
