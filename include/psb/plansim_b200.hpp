@@ -194,6 +194,14 @@ std::vector<ParallelScheme> enumerate_schemes(const ModelSpec& model, const Bloc
 std::vector<ExecutionPlan> generate_plans(const ModelSpec& model, const BlockSpec& block,
                                           const ClusterSpec& cluster,
                                           const PlanOptions& opts = {});
+class Engine;
+// generate_plans with the device mapping, collective resolution and memory
+// ledger of every candidate computed on the GPU (psg_plan_compute; SURVEY.md
+// §8(f) row 3); the same plans, field for field.
+std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& model, const BlockSpec& block,
+                                                 const ClusterSpec& cluster,
+                                                 const PlanOptions& opts = {},
+                                                 Engine* engine = nullptr);
 ExecutionPlan build_plan(const ModelSpec& model, const BlockSpec& block,
                          const ClusterSpec& cluster, int model_dp, int num_stages,
                          const std::vector<CellChoice>& cells, const PlanOptions& opts = {});

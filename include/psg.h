@@ -280,6 +280,47 @@ typedef struct psg_synth_grid {
   double hidden, head_dim, kv_elems;  /* GridSpec::shape */
 } psg_synth_grid;
 
+/* Plan enumeration / device mapping on the device (generate_plans,
+   planner.cpp:188-389): the host lists the candidate groups (model_dp,
+   stages) with their per-cell scheme choices (enumerate_schemes order); the
+   device maps each group onto the cluster (map_devices, cluster.cpp:118-198),
+   and for every candidate (one per choice combination, last cell fastest)
+   resolves the reshard collectives against that mapping (worst group span)
+   and computes the memory ledger (finalize_plan, planner.cpp:307-370). */
+#define PSG_PLAN_MAX_CELLS 8
+#define PSG_PLAN_MAX_COLLS (2 * PSG_PLAN_MAX_CELLS)
+typedef struct psg_plan_space {
+  int32_t n_devices, per_node, n_levels;
+  const int32_t* subtree_cap;         /* [n_levels + 1] devices per subtree of each level */
+  double memory_capacity, activation_reserve, emb_bytes, kv_elem_bytes;
+  int32_t include_embedding, num_layers, n_cells;
+  const int32_t* cell_is_attention;   /* [n_cells] */
+  const double* cell_kv_heads;        /* [n_cells] */
+  const double* cell_head_dim;        /* [n_cells] */
+  int32_t n_groups;
+  const int32_t* group_dp;            /* [n_groups] */
+  const int32_t* group_stages;
+  const int32_t* group_sdev;          /* devices per stage */
+  const int32_t* group_reps;          /* stage repetitions */
+  const int64_t* group_first;         /* [n_groups + 1] candidate ranges */
+  const int32_t* choice_begin;        /* [n_groups * n_cells + 1] */
+  const int32_t* ch_mode;             /* per choice: CellScheme mode (0 TP, 1 EP), cell_dp, intra */
+  const int32_t* ch_cdp;
+  const int32_t* ch_intra;
+  const double* ch_weight;            /* weight_bytes_per_device */
+} psg_plan_space;
+
+typedef struct psg_plan_record {
+  int32_t feasible;                   /* static_bytes_per_device <= memory capacity */
+  int32_t n_colls;
+  double static_bytes_per_device, kv_budget_per_replica, kv_bytes_per_token;
+  int32_t coll_kind[PSG_PLAN_MAX_COLLS];   /* PSG_COLL_* */
+  int32_t coll_devices[PSG_PLAN_MAX_COLLS];
+  int32_t coll_nodes[PSG_PLAN_MAX_COLLS];
+  int32_t coll_groups[PSG_PLAN_MAX_COLLS];
+  double coll_share[PSG_PLAN_MAX_COLLS];
+} psg_plan_record;
+
 typedef struct psg_context psg_context;
 
 const char* psg_version(void);
@@ -292,6 +333,12 @@ const char* psg_last_error(const psg_context* ctx);
 /* seconds / joules: n_variants * 3 * n_ctx * n_tasks * n_width values each. */
 int psg_synth_compute(psg_context* ctx, const psg_synth_grid* grid, double* seconds,
                       double* joules);
+
+/* records: group_first[n_groups] entries; phys: [n_groups * n_devices]
+   assignment ((r * stages + s) * stage_devices + slot); p2p: per group
+   stages - 1 boundary node counts at p2p_offset[g] ([n_groups + 1]). */
+int psg_plan_compute(psg_context* ctx, const psg_plan_space* space, psg_plan_record* records,
+                     int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
 
 /* Evaluate-all-plans: plansim::search semantics (see header comment). */
 int psg_search(psg_context* ctx, const psg_plan_set* plans,

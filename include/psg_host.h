@@ -47,6 +47,8 @@ int psgh_trace_synth(psgh_problem* p, double ctx_mean, double ctx_std, double ge
 int psgh_trace_load(psgh_problem* p, const char* jsonl);
 /* generate_plans(): replaces the problem's plan list. */
 int psgh_plans_generate(psgh_problem* p);
+/* The same plans with the candidates mapped and finalized on the GPU. */
+int psgh_plans_generate_device(psgh_problem* p);
 /* build_plan(): appends one plan; modes[i] is 0 (TP) or 1 (EP). */
 int psgh_plan_build(psgh_problem* p, int model_dp, int num_stages, int n_cells,
                     const int32_t* modes, const int32_t* cell_dp, const int32_t* intra);

@@ -139,6 +139,13 @@ int psgh_plans_generate(psgh_problem* p) {
   });
 }
 
+int psgh_plans_generate_device(psgh_problem* p) {
+  return guarded([&] {
+    p->plans = psb::generate_plans_device(p->model, p->block, p->cluster, p->opts);
+    p->soa.reset();
+  });
+}
+
 int psgh_plan_build(psgh_problem* p, int dp, int stages, int n_cells, const int32_t* modes,
                     const int32_t* cell_dp, const int32_t* intra) {
   return guarded([&] {

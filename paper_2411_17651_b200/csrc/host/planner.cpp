@@ -5,6 +5,7 @@
 // tests/test_host_planner.py.
 #include <algorithm>
 #include <iostream>
+#include <memory>
 #include <set>
 #include <sstream>
 
@@ -280,6 +281,165 @@ std::vector<ExecutionPlan> generate_plans(const ModelSpec& m, const BlockSpec& b
   for (const auto& sch : enumerate_schemes(m, block, cl.total_devices(), opts.max_cell_combinations)) {
     ExecutionPlan p = finalize(m, sch, cl, opts);
     if (p.static_bytes_per_device <= cl.device.memory_capacity) plans.push_back(std::move(p));
+  }
+  if (plans.empty()) throw InfeasibleError("no parallel execution plan fits the model on this cluster");
+  return plans;
+}
+
+std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const BlockSpec& block,
+                                                 const ClusterSpec& cl, const PlanOptions& opts,
+                                                 Engine* engine) {
+  // Candidate groups and per-cell choices exactly as enumerate_schemes lists
+  // them; the device maps every group and finalizes every candidate.
+  const int n = cl.total_devices();
+  const int nc = int(block.cells.size());
+  if (nc < 1 || nc > PSG_PLAN_MAX_CELLS) throw DataError("plan space: unsupported cell count");
+  struct Group {
+    int dp, stages, sdev;
+    std::vector<std::vector<CellScheme>> choices;
+    long long combos;
+  };
+  std::vector<Group> groups;
+  if (n >= 1 && block.repeat_count >= 1) {
+    for (const int dp : divisors(n)) {
+      const int per_replica = n / dp;
+      for (const int stages : divisors(per_replica)) {
+        if (stages > block.repeat_count || block.repeat_count % stages) continue;
+        const int sd = per_replica / stages;
+        Group g{dp, stages, sd, std::vector<std::vector<CellScheme>>(static_cast<size_t>(nc)), 1};
+        bool viable = true;
+        for (int ci = 0; ci < nc && viable; ++ci) {
+          for (const int cdp : divisors(sd)) {
+            const int intra = sd / cdp;
+            if (template_valid(block.cells[size_t(ci)], intra, ParallelMode::TP))
+              g.choices[size_t(ci)].push_back(cell_scheme(block.cells[size_t(ci)], ParallelMode::TP, cdp, intra));
+            if (intra > 1 && template_valid(block.cells[size_t(ci)], intra, ParallelMode::EP))
+              g.choices[size_t(ci)].push_back(cell_scheme(block.cells[size_t(ci)], ParallelMode::EP, cdp, intra));
+          }
+          viable = !g.choices[size_t(ci)].empty();
+        }
+        if (!viable) continue;
+        for (const auto& c : g.choices) g.combos *= (long long)c.size();
+        if (g.combos > opts.max_cell_combinations) {
+          std::cerr << "warning: capping cell-scheme combinations at " << opts.max_cell_combinations
+                    << " (of " << g.combos << ") for dp=" << dp << " stages=" << stages << "\n";
+          g.combos = opts.max_cell_combinations;
+        }
+        groups.push_back(std::move(g));
+      }
+    }
+  }
+  const int G = int(groups.size());
+  std::vector<int32_t> subtree(static_cast<size_t>(cl.num_levels()) + 1), att(static_cast<size_t>(nc)),
+      gdp, gst, gsd, grp, cb, cm, cd, ci_;
+  std::vector<double> kvh(static_cast<size_t>(nc)), hd(static_cast<size_t>(nc)), cw;
+  std::vector<int64_t> gfirst{0}, p2p_off{0};
+  for (int l = 0; l <= cl.num_levels(); ++l) subtree[size_t(l)] = cl.subtree_capacity(l);
+  for (int i = 0; i < nc; ++i) {
+    att[size_t(i)] = block.cells[size_t(i)].is_attention() ? 1 : 0;
+    kvh[size_t(i)] = double(block.cells[size_t(i)].kv_heads);
+    hd[size_t(i)] = block.cells[size_t(i)].head_dim;
+  }
+  for (const Group& g : groups) {
+    gdp.push_back(g.dp);
+    gst.push_back(g.stages);
+    gsd.push_back(g.sdev);
+    grp.push_back(block.repeat_count / g.stages);
+    gfirst.push_back(gfirst.back() + g.combos);
+    p2p_off.push_back(p2p_off.back() + (g.stages - 1));
+    for (const auto& opts_c : g.choices) {
+      cb.push_back(int32_t(cm.size()));
+      for (const CellScheme& c : opts_c) {
+        cm.push_back(c.mode == ParallelMode::EP ? 1 : 0);
+        cd.push_back(c.cell_dp);
+        ci_.push_back(c.intra_degree);
+        cw.push_back(c.weight_bytes_per_device);
+      }
+    }
+  }
+  cb.push_back(int32_t(cm.size()));
+  psg_plan_space sp{};
+  sp.n_devices = n;
+  sp.per_node = cl.devices_per_node();
+  sp.n_levels = cl.num_levels();
+  sp.subtree_cap = subtree.data();
+  sp.memory_capacity = cl.device.memory_capacity;
+  sp.activation_reserve = opts.activation_reserve;
+  sp.emb_bytes = embedding_weight_bytes(m);
+  sp.kv_elem_bytes = m.kv_cache_dtype.bytes_per_element;
+  sp.include_embedding = opts.include_embedding ? 1 : 0;
+  sp.num_layers = m.num_layers;
+  sp.n_cells = nc;
+  sp.cell_is_attention = att.data();
+  sp.cell_kv_heads = kvh.data();
+  sp.cell_head_dim = hd.data();
+  sp.n_groups = G;
+  sp.group_dp = gdp.data();
+  sp.group_stages = gst.data();
+  sp.group_sdev = gsd.data();
+  sp.group_reps = grp.data();
+  sp.group_first = gfirst.data();
+  sp.choice_begin = cb.data();
+  sp.ch_mode = cm.data();
+  sp.ch_cdp = cd.data();
+  sp.ch_intra = ci_.data();
+  sp.ch_weight = cw.data();
+  std::vector<psg_plan_record> rec(static_cast<size_t>(std::max<int64_t>(gfirst.back(), 1)));
+  std::vector<int32_t> phys(static_cast<size_t>(std::max(G, 1)) * static_cast<size_t>(n));
+  std::vector<int32_t> p2p(static_cast<size_t>(std::max<int64_t>(p2p_off.back(), 1)));
+  std::unique_ptr<Engine> own;
+  if (!engine) {
+    own = std::make_unique<Engine>(0);
+    engine = own.get();
+  }
+  if (G > 0) {
+    const int rc = psg_plan_compute(engine->handle(), &sp, rec.data(), phys.data(), p2p_off.data(), p2p.data());
+    if (rc != PSG_OK) throw DataError(std::string("plan space on device: ") + psg_last_error(engine->handle()));
+  }
+  std::vector<ExecutionPlan> plans;
+  std::set<std::string> seen;
+  const double per_token = double(m.hidden_size) * m.activation_dtype.bytes_per_element;
+  for (int gi = 0; gi < G; ++gi) {
+    const Group& g = groups[size_t(gi)];
+    std::vector<size_t> digit(static_cast<size_t>(nc), 0);
+    for (long long k = 0; k < g.combos; ++k) {
+      std::vector<CellScheme> cells;
+      for (int c = 0; c < nc; ++c) cells.push_back(g.choices[size_t(c)][digit[size_t(c)]]);
+      ParallelScheme sch = assemble(m, block, g.dp, g.stages, g.sdev, std::move(cells));
+      const psg_plan_record& r = rec[size_t(gfirst[size_t(gi)] + k)];
+      if (seen.insert(sch.encoding).second && r.feasible) {
+        ExecutionPlan p;
+        p.scheme = std::move(sch);
+        p.assignment.model_dp = g.dp;
+        p.assignment.num_stages = g.stages;
+        p.assignment.stage_devices = g.sdev;
+        p.assignment.phys.assign(phys.begin() + size_t(gi) * n, phys.begin() + size_t(gi + 1) * n);
+        p.compute_dtype = m.activation_dtype.name;
+        p.op_shape.model_hidden = m.hidden_size;
+        p.op_shape.head_dim = m.head_dim;
+        p.op_shape.kv_elems_per_task_token = 2.0 * m.head_dim / (m.num_attention_heads / double(m.num_kv_heads));
+        p.p2p_payload_per_token = per_token;
+        for (int q = 0; q < r.n_colls; ++q) {
+          ResolvedCollective rc;
+          rc.kind = CollectiveKind(r.coll_kind[q]);
+          rc.payload_bytes_per_token = per_token;
+          rc.token_share = r.coll_share[q];
+          rc.num_devices = r.coll_devices[q];
+          rc.num_nodes = r.coll_nodes[q];
+          rc.groups_per_stage = r.coll_groups[q];
+          p.block_collectives.push_back(rc);
+        }
+        p.p2p_boundary_nodes.assign(p2p.begin() + p2p_off[size_t(gi)], p2p.begin() + p2p_off[size_t(gi) + 1]);
+        p.static_bytes_per_device = r.static_bytes_per_device;
+        p.kv_budget_per_replica = r.kv_budget_per_replica;
+        p.kv_bytes_per_token = r.kv_bytes_per_token;
+        plans.push_back(std::move(p));
+      }
+      for (size_t c = digit.size(); c-- > 0;) {
+        if (++digit[c] < g.choices[c].size()) break;
+        digit[c] = 0;
+      }
+    }
   }
   if (plans.empty()) throw InfeasibleError("no parallel execution plan fits the model on this cluster");
   return plans;

@@ -132,7 +132,7 @@ struct psg_context {
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
-  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth;
+  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
   std::vector<uint8_t> compute_clamp, curve_clamp;
@@ -200,6 +200,80 @@ int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, do
   return PSG_OK;
 }
 
+int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
+                 int32_t* phys, const int64_t* p2p_offset, int32_t* p2p) {
+  if (!ctx || !s || !records || !phys || !p2p_offset || !p2p) return PSG_ERR_USAGE;
+  const int n = s->n_devices, G = s->n_groups, nc = s->n_cells;
+  if (n < 1 || G < 0 || nc < 1 || nc > PSG_PLAN_MAX_CELLS || s->n_levels < 1)
+    return fail(ctx, PSG_ERR_USAGE, "plan space: bad sizes");
+  if (G == 0) return PSG_OK;
+  const int64_t total = s->group_first[G];
+  const int64_t n_choice = s->choice_begin[int64_t(G) * nc];
+  const int64_t n_p2p = p2p_offset[G];
+  const size_t map_smem = size_t(n) * (sizeof(int32_t) + 1);
+  if (map_smem > size_t(ctx->smem_block_max)) return fail(ctx, PSG_ERR_USAGE, "plan space: too many devices");
+  PSG_CUDA(cudaSetDevice(ctx->device));
+  Packer pk;
+  const size_t o_cap = pk.add(s->subtree_cap, size_t(s->n_levels) + 1),
+               o_att = pk.add(s->cell_is_attention, size_t(nc)), o_kvh = pk.add(s->cell_kv_heads, size_t(nc)),
+               o_hd = pk.add(s->cell_head_dim, size_t(nc)), o_gdp = pk.add(s->group_dp, size_t(G)),
+               o_gst = pk.add(s->group_stages, size_t(G)), o_gsd = pk.add(s->group_sdev, size_t(G)),
+               o_grp = pk.add(s->group_reps, size_t(G)), o_gfi = pk.add(s->group_first, size_t(G) + 1),
+               o_cb = pk.add(s->choice_begin, size_t(G) * nc + 1), o_cm = pk.add(s->ch_mode, size_t(n_choice)),
+               o_cd = pk.add(s->ch_cdp, size_t(n_choice)), o_ci = pk.add(s->ch_intra, size_t(n_choice)),
+               o_cw = pk.add(s->ch_weight, size_t(n_choice)), o_p2o = pk.add(p2p_offset, size_t(G) + 1);
+  const size_t in_bytes = (pk.size + 15) & ~size_t(15);
+  const size_t rec_bytes = sizeof(psg_plan_record) * size_t(std::max<int64_t>(total, 1));
+  const size_t phys_bytes = sizeof(int32_t) * size_t(G) * n;
+  const size_t p2p_bytes = sizeof(int32_t) * size_t(std::max<int64_t>(n_p2p, 1));
+  const size_t span_bytes = sizeof(int32_t) * size_t(G) * (n + 1);
+  const size_t o_rec = in_bytes, o_phys = o_rec + ((rec_bytes + 15) & ~size_t(15)),
+               o_p2p = o_phys + ((phys_bytes + 15) & ~size_t(15)),
+               o_sn = o_p2p + ((p2p_bytes + 15) & ~size_t(15)),
+               o_sl = o_sn + ((span_bytes + 15) & ~size_t(15)), tot = o_sl + span_bytes;
+  PSG_CUDA(ctx->d_plan.ensure(tot));
+  PSG_CUDA(ctx->h_in.ensure(in_bytes));
+  pk.write(static_cast<unsigned char*>(ctx->h_in.p));
+  auto* d = static_cast<unsigned char*>(ctx->d_plan.p);
+  PSG_CUDA(cudaMemcpyAsync(d, ctx->h_in.p, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  psg_plan_space ds = *s;
+  ds.subtree_cap = reinterpret_cast<const int32_t*>(d + o_cap);
+  ds.cell_is_attention = reinterpret_cast<const int32_t*>(d + o_att);
+  ds.cell_kv_heads = reinterpret_cast<const double*>(d + o_kvh);
+  ds.cell_head_dim = reinterpret_cast<const double*>(d + o_hd);
+  ds.group_dp = reinterpret_cast<const int32_t*>(d + o_gdp);
+  ds.group_stages = reinterpret_cast<const int32_t*>(d + o_gst);
+  ds.group_sdev = reinterpret_cast<const int32_t*>(d + o_gsd);
+  ds.group_reps = reinterpret_cast<const int32_t*>(d + o_grp);
+  ds.group_first = reinterpret_cast<const int64_t*>(d + o_gfi);
+  ds.choice_begin = reinterpret_cast<const int32_t*>(d + o_cb);
+  ds.ch_mode = reinterpret_cast<const int32_t*>(d + o_cm);
+  ds.ch_cdp = reinterpret_cast<const int32_t*>(d + o_cd);
+  ds.ch_intra = reinterpret_cast<const int32_t*>(d + o_ci);
+  ds.ch_weight = reinterpret_cast<const double*>(d + o_cw);
+  auto* d_rec = reinterpret_cast<psg_plan_record*>(d + o_rec);
+  auto* d_phys = reinterpret_cast<int32_t*>(d + o_phys);
+  auto* d_p2p = reinterpret_cast<int32_t*>(d + o_p2p);
+  auto* d_sn = reinterpret_cast<int32_t*>(d + o_sn);
+  auto* d_sl = reinterpret_cast<int32_t*>(d + o_sl);
+  if (map_smem > 48 * 1024)
+    PSG_CUDA(cudaFuncSetAttribute(plan_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(map_smem)));
+  plan_map_kernel<<<G, 128, map_smem, ctx->stream>>>(ds, d_phys, reinterpret_cast<const int64_t*>(d + o_p2o),
+                                                     d_p2p, d_sn, d_sl);
+  PSG_CUDA(cudaGetLastError());
+  if (total > 0) {
+    plan_candidate_kernel<<<unsigned((total + 127) / 128), 128, 0, ctx->stream>>>(ds, d_sn, d_rec);
+    PSG_CUDA(cudaGetLastError());
+    PSG_CUDA(cudaMemcpyAsync(records, d_rec, sizeof(psg_plan_record) * size_t(total), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  }
+  PSG_CUDA(cudaMemcpyAsync(phys, d_phys, phys_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (n_p2p > 0)
+    PSG_CUDA(cudaMemcpyAsync(p2p, d_p2p, sizeof(int32_t) * size_t(n_p2p), cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return PSG_OK;
+}
+
 }  // namespace psg
 
 extern "C" {
@@ -248,7 +322,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
                     &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
-                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth})
+                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj, &ctx->h_it, &ctx->h_isec, &ctx->h_ijou})
     b->release();

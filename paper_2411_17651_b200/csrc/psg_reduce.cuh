@@ -41,6 +41,12 @@ struct ReduceParams {
 
 __global__ void synth_compute_kernel(const psg_synth_grid g, double* sec, double* jou);
 int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, double* joules);
+__global__ void plan_map_kernel(const psg_plan_space s, int32_t* phys_out, const int64_t* p2p_off,
+                                int32_t* p2p_out, int32_t* span_nodes, int32_t* span_level);
+__global__ void plan_candidate_kernel(const psg_plan_space s, const int32_t* span_nodes,
+                                      psg_plan_record* out);
+int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
+                 int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
 __global__ void sim_kernel(const SimParams p);       // one warp per block
 __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per block
 __global__ void entry_reduce_kernel(const ReduceParams r);

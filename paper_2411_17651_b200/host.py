@@ -39,6 +39,7 @@ def _lib():
                                      C.c_double, C.c_int64, C.c_uint64]
     lib.psgh_trace_load.argtypes = [v, C.c_char_p]
     lib.psgh_plans_generate.argtypes = [v]
+    lib.psgh_plans_generate_device.argtypes = [v]
     lib.psgh_plan_build.argtypes = [v, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     lib.psgh_plans_count.argtypes = [v]
@@ -117,8 +118,11 @@ class Problem:
         self._check(self.lib.psgh_trace_load(self.h, jsonl.encode()))
         return self
 
-    def generate_plans(self):
-        self._check(self.lib.psgh_plans_generate(self.h))
+    def generate_plans(self, device=False):
+        """generate_plans (planner.cpp:375-389); device=True maps and finalizes
+        the candidates on the GPU (the same plans, field for field)."""
+        fn = self.lib.psgh_plans_generate_device if device else self.lib.psgh_plans_generate
+        self._check(fn(self.h))
         return self
 
     def build_plan(self, model_dp, num_stages, cells):
