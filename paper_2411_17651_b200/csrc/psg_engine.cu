@@ -773,7 +773,13 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
   sp.tab_smem = tab_smem;
   sp.chain_replicas = 1;
   if (const char* v = std::getenv("PSG_CHAIN_REPLICAS")) sp.chain_replicas = std::atoi(v) != 0;  // dev knob
-  sp.speculate = 1;
+  {
+    // The speculation warps pay off while they get SM sub-partitions of their
+    // own: with more than ~1.5 simulation blocks per SM they share them with
+    // other blocks' simulation warps and slow those down (C5: 2 blocks / SM).
+    const int blocks = std::max(sp.chain_replicas ? E : n_units, ctx->concurrent_blocks);
+    sp.speculate = 2 * int64_t(blocks) <= 3 * int64_t(ctx->n_sm) ? 1 : 0;
+  }
   if (const char* v = std::getenv("PSG_SPECULATE")) sp.speculate = std::atoi(v);  // dev knob: 0 off, 2 idle helper
   sp.spec_sleep_ns = 20;
   if (const char* v = std::getenv("PSG_SPEC_SLEEP_NS")) sp.spec_sleep_ns = std::max(0, std::atoi(v));  // dev knob

@@ -47,7 +47,8 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 // Phase profiler (dev builds only: -DPSG_PHASE_PROFILE; zero code otherwise).
 // slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 decode cost,
 // 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
-// 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 #speculation hits, 15 total.
+// 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 #speculation hits, 15 total,
+// 16 cycles waited for speculation results, 17 eval cycles of misses.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -759,8 +760,10 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       }
       if (use_spec) {
         PROF_CNT(14);
+        PROF_T0(t_wait);
         while (unsigned(vload(s_spec.done)) != spec_seq) {
         }
+        PROF_ADD(16, t_wait);
         __threadfence_block();
         ev.cd = s_spec.cd;
         ev.ce = s_spec.ce;
@@ -770,9 +773,11 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         spec_tok = -1;
         __syncwarp();
       } else {
+        PROF_T0(t_own);
         ev = eval_iteration(
             ectx, lane, [&](int i) { return a.items[i]; }, n_items, decode, total, cellq, cdesc,
             tab, p2p_slot, qv, p2p_val);
+        PROF_ADD(17, t_own);
       }
       const double srep = ev.srep, jrep = ev.jrep;
       const double cd = ev.cd, ce = ev.ce, cf = ev.cf, cb = ev.cb;

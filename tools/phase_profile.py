@@ -18,7 +18,8 @@ sys.path.insert(0, os.path.join(REPO, "oracle"))
 sys.path.insert(0, os.path.join(REPO, "tests"))
 
 NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
-         "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total"]
+         "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total",
+         "spec_wait_cyc", "miss_eval_cyc"]
 
 
 def main():
@@ -42,8 +43,18 @@ def run(key, args):
     case = RefCase(args.key, args.workdir)
     eng = Engine(0)
     res = eng.search(case.plans, case.cluster, case.store, case.trace, case.config())
-    raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 18)
+    raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 20)
     meta, cnt = raw[:, :2].view(np.int64), raw[:, 2:]
+    if os.environ.get("PSG_CHAIN_REPLICAS", "1") != "0":
+        # replicas of an entry run in order on one warp: aggregate per entry
+        ents = np.unique(meta[:, 0])
+        agg = np.zeros((len(ents), cnt.shape[1]), dtype=np.uint64)
+        m2 = np.zeros((len(ents), 2), dtype=np.int64)
+        for i, e in enumerate(ents):
+            rows = meta[:, 0] == e
+            agg[i] = cnt[rows].sum(axis=0)
+            m2[i] = (e, -int(rows.sum()))  # replica column: -(number of replicas)
+        meta, cnt = m2, agg
     order = np.argsort(-cnt[:, 15].astype(np.float64))
     F = max(1, len(case.workload.freqs))
     tots = cnt[:, 15].astype(np.float64)
@@ -55,6 +66,8 @@ def run(key, args):
         enc = case.plans.encodings[int(meta[u, 0]) // F]
         parts = " ".join(f"{NAMES[k]}={100 * cnt[u, k] / tot:.1f}%" for k in range(10))
         counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 15))
+        hits, miss = max(1, int(cnt[u, 14])), max(1, int(cnt[u, 10]) - int(cnt[u, 14]))
+        counts += f" | wait/hit={int(cnt[u, 16]) // hits} cyc, eval/miss={int(cnt[u, 17]) // miss} cyc"
         print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
 
 
