@@ -75,9 +75,9 @@ __device__ __forceinline__ int64_t nearest_rank(double q, int64_t n) {
 
 __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r) {
   const int e = blockIdx.x;
-  __shared__ unsigned hist[256];
-  __shared__ uint64_t sh_prefix;
-  __shared__ int64_t sh_k;
+  __shared__ unsigned sel_hist[5][256];
+  __shared__ uint64_t sel_prefix[5];
+  __shared__ int64_t sel_k[5];
   __shared__ double sh_sums[2];
   __shared__ int64_t sh_cnt[2];
 
@@ -94,34 +94,52 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
     if (st[i] == 1) tpot[i] = gen[i] >= 2 ? __ddiv_rn(tpot[i], double(gen[i] - 1)) : 0.0;
   __syncthreads();
 
-  // ---- ordered means: one serial chain in ascending id order (warp 0) ----
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double ts = 0.0, ps = 0.0;
-    int64_t pn = 0, cn = 0;
-    for (int64_t b0 = 0; b0 < r.n_slots; b0 += 32) {
-      const int64_t i = b0 + lane;
-      const bool c = i < r.n_slots && st[i] == 1;
-      const double tv = c ? ttft[i] : 0.0;
-      const bool g2 = c && gen[i] >= 2;
-      const double pv = g2 ? tpot[i] : 0.0;
-      unsigned cm = __ballot_sync(0xffffffffu, c);
-      const unsigned gm = __ballot_sync(0xffffffffu, g2);
-      cn += __popc(cm);
-      pn += __popc(gm);
-      while (cm) {
-        const int l = __ffs(cm) - 1;
-        cm &= cm - 1;
-        ts = __dadd_rn(ts, __shfl_sync(0xffffffffu, tv, l));
-        if ((gm >> l) & 1u) ps = __dadd_rn(ps, __shfl_sync(0xffffffffu, pv, l));
+  // ---- ordered means: one serial chain in ascending id order ----
+  // The block stages tiles of the slot arrays in shared memory (coalesced),
+  // thread 0 runs the chain from there.  A slot that does not count adds
+  // +0.0, which leaves the non-negative (never -0) sums bit-identical, so the
+  // chain needs no branches.
+  constexpr int kTile = 1024;
+  __shared__ double tile_t[kTile], tile_p[kTile];
+  __shared__ unsigned char tile_c[kTile], tile_g[kTile];
+  double ts = 0.0, ps = 0.0;
+  int64_t pn = 0, cn = 0;
+  for (int64_t b0 = 0; b0 < r.n_slots; b0 += kTile) {
+    const int len = int(min(int64_t(kTile), r.n_slots - b0));
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const int64_t q = b0 + i;
+      const bool c = st[q] == 1, g2 = c && gen[q] >= 2;
+      tile_c[i] = c;
+      tile_g[i] = g2;
+      tile_t[i] = c ? ttft[q] : 0.0;
+      tile_p[i] = g2 ? tpot[q] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int i = 0;
+      for (; i + 8 <= len; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ts = __dadd_rn(ts, tile_t[i + u]);
+          ps = __dadd_rn(ps, tile_p[i + u]);
+          cn += tile_c[i + u];
+          pn += tile_g[i + u];
+        }
+      }
+      for (; i < len; ++i) {
+        ts = __dadd_rn(ts, tile_t[i]);
+        ps = __dadd_rn(ps, tile_p[i]);
+        cn += tile_c[i];
+        pn += tile_g[i];
       }
     }
-    if (lane == 0) {
-      sh_sums[0] = ts;
-      sh_sums[1] = ps;
-      sh_cnt[0] = cn;
-      sh_cnt[1] = pn;
-    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sh_sums[0] = ts;
+    sh_sums[1] = ps;
+    sh_cnt[0] = cn;
+    sh_cnt[1] = pn;
   }
   __syncthreads();
   const int64_t ncomp = sh_cnt[0], ntpot = sh_cnt[1];
@@ -173,19 +191,85 @@ __global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r)
     }
   }
 
-  // ---- order statistics ----
+  // ---- order statistics: p95 latency (simulator.cpp:222-225) and the
+  // p50/p99 TTFT/TPOT extras, all five by one fused MSB radix select: each
+  // 8-bit pass sweeps the slots once and builds the five histograms, one
+  // warp per statistic picks its digit ----
   double p95 = 0.0, t50 = 0.0, t99 = 0.0, q50 = 0.0, q99 = 0.0;
   if (ncomp > 0) {
-    auto done = [&](int64_t i) { return st[i] == 1; };
-    auto done2 = [&](int64_t i) { return st[i] == 1 && gen[i] >= 2; };
-    p95 = block_select(e2e, r.n_slots, nearest_rank(0.95, ncomp), done, hist, &sh_prefix, &sh_k);
-    if (r.extras) {
-      t50 = block_select(ttft, r.n_slots, nearest_rank(0.50, ncomp), done, hist, &sh_prefix, &sh_k);
-      t99 = block_select(ttft, r.n_slots, nearest_rank(0.99, ncomp), done, hist, &sh_prefix, &sh_k);
-      if (ntpot > 0) {
-        q50 = block_select(tpot, r.n_slots, nearest_rank(0.50, ntpot), done2, hist, &sh_prefix, &sh_k);
-        q99 = block_select(tpot, r.n_slots, nearest_rank(0.99, ntpot), done2, hist, &sh_prefix, &sh_k);
+    const int m = r.extras ? (ntpot > 0 ? 5 : 3) : 1;
+    if (threadIdx.x < 5) {
+      const int j = threadIdx.x;
+      sel_k[j] = j == 0 ? nearest_rank(0.95, ncomp)
+               : j == 1 ? nearest_rank(0.50, ncomp)
+               : j == 2 ? nearest_rank(0.99, ncomp)
+               : j == 3 ? nearest_rank(0.50, ntpot > 0 ? ntpot : 1)
+                        : nearest_rank(0.99, ntpot > 0 ? ntpot : 1);
+      sel_prefix[j] = 0;
+    }
+    uint64_t mask = 0;
+    for (int pass = 7; pass >= 0; --pass) {
+      const int shift = pass * 8;
+      for (int i = threadIdx.x; i < 5 * 256; i += blockDim.x) sel_hist[i / 256][i % 256] = 0;
+      __syncthreads();
+      const uint64_t pe = sel_prefix[0], pt50 = sel_prefix[1], pt99 = sel_prefix[2],
+                     pp50 = sel_prefix[3], pp99 = sel_prefix[4];
+      for (int64_t i = threadIdx.x; i < r.n_slots; i += blockDim.x) {
+        if (st[i] != 1) continue;
+        const uint64_t ke = order_key(e2e[i]) , m8 = (ke >> shift) & 255u;
+        if ((ke & mask) == pe) atomicAdd(&sel_hist[0][m8], 1u);
+        if (m > 1) {
+          const uint64_t kt = order_key(ttft[i]), d = (kt >> shift) & 255u;
+          if ((kt & mask) == pt50) atomicAdd(&sel_hist[1][d], 1u);
+          if ((kt & mask) == pt99) atomicAdd(&sel_hist[2][d], 1u);
+          if (m > 3 && gen[i] >= 2) {
+            const uint64_t kp = order_key(tpot[i]), dp = (kp >> shift) & 255u;
+            if ((kp & mask) == pp50) atomicAdd(&sel_hist[3][dp], 1u);
+            if ((kp & mask) == pp99) atomicAdd(&sel_hist[4][dp], 1u);
+          }
+        }
       }
+      __syncthreads();
+      const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+      if (w < m) {  // first digit whose inclusive count exceeds k (as the serial scan)
+        const int64_t k = sel_k[w];
+        unsigned part = 0;
+        for (int b = 0; b < 8; ++b) part += sel_hist[w][lane * 8 + b];
+        unsigned incl = part;
+        for (int off = 1; off < 32; off <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        const int64_t excl = int64_t(incl - part);
+        const bool here = excl <= k && k < excl + int64_t(part);
+        const unsigned hm = __ballot_sync(0xffffffffu, here);
+        if (hm) {
+          if (lane == __ffs(hm) - 1) {
+            int64_t kk = k - excl;
+            int d = lane * 8;
+            for (; d < lane * 8 + 7; ++d) {
+              if (kk < int64_t(sel_hist[w][d])) break;
+              kk -= sel_hist[w][d];
+            }
+            sel_k[w] = kk;
+            sel_prefix[w] |= uint64_t(d) << shift;
+          }
+        } else if (lane == 31) {  // k beyond every count: digit 255, as the serial scan
+          sel_k[w] = k - (excl + int64_t(part) - int64_t(sel_hist[w][255]));
+          sel_prefix[w] |= uint64_t(255) << shift;
+        }
+      }
+      mask |= uint64_t(255) << shift;
+      __syncthreads();
+    }
+    p95 = from_order_key(sel_prefix[0]);
+    if (m > 1) {
+      t50 = from_order_key(sel_prefix[1]);
+      t99 = from_order_key(sel_prefix[2]);
+    }
+    if (m > 3) {
+      q50 = from_order_key(sel_prefix[3]);
+      q99 = from_order_key(sel_prefix[4]);
     }
   }
   if (threadIdx.x == 0) {
