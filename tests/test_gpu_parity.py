@@ -42,7 +42,7 @@ def test_search_matches_reference(engine, workdir, key, extra):
 
 @pytest.mark.slow
 @pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
-@pytest.mark.parametrize("key", ["c2", "c2fp8"])
+@pytest.mark.parametrize("key", ["c2", "c2fp8", "c5_10k"])
 def test_c2_matches_reference(engine, workdir, key):
     case = RefCase(key, workdir)
     res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
