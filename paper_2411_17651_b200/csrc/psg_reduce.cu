@@ -4,8 +4,8 @@
 //                       e2e = max over replicas, energy summed in replica
 //                       order, mean TTFT/TPOT summed in ascending-id order
 //                       (one serial FP64 chain, as the reference), p95 by
-//                       nearest rank via an MSB radix select, MFU/MBU; plus
-//                       the additive p50/p99 TTFT/TPOT outputs.
+//                       nearest rank via a fused MSB radix select (also the
+//                       additive p50/p99 TTFT/TPOT outputs), MFU/MBU.
 //  compact_kernel       per_request sorted by id / rejected_ids sorted
 //                       (simulator.cpp:205-207) as dense arrays for one D2H.
 //  rank_kernel          search()'s comparator (simulator.cpp:283-294):
@@ -26,42 +26,6 @@ __device__ __forceinline__ uint64_t order_key(double v) {
 __device__ __forceinline__ double from_order_key(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double(b);
-}
-
-// k-th smallest (0-based) value among slots passing `pred`, by 8 MSB-first
-// 8-bit radix passes with a shared histogram.  All threads of the CTA call it.
-template <typename Pred>
-__device__ double block_select(const double* __restrict__ v, int64_t n, int64_t k,
-                               Pred pred, unsigned* hist, uint64_t* shared_prefix,
-                               int64_t* shared_k) {
-  uint64_t prefix = 0, mask = 0;
-  if (threadIdx.x == 0) *shared_k = k;
-  for (int pass = 7; pass >= 0; --pass) {
-    const int shift = pass * 8;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      if (!pred(i)) continue;
-      const uint64_t key = order_key(v[i]);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t kk = *shared_k;
-      int d = 0;
-      for (; d < 255; ++d) {
-        if (kk < int64_t(hist[d])) break;
-        kk -= hist[d];
-      }
-      *shared_k = kk;
-      *shared_prefix = prefix | (uint64_t(d) << shift);
-    }
-    __syncthreads();
-    prefix = *shared_prefix;
-    mask |= uint64_t(255) << shift;
-    __syncthreads();
-  }
-  return from_order_key(prefix);
 }
 
 // Nearest-rank index of simulator.cpp:224-225.
