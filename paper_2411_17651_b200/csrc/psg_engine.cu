@@ -492,6 +492,11 @@ int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
     slot[slot_order[s]] = int32_t(s);
     slot_id[s] = T->id[slot_order[s]];
     slot_gen[s] = T->gen_len[slot_order[s]];
+    // the reference keys per-request state by id (simulator.cpp:103-110):
+    // repeated ids blend metrics and leave the per-request order unspecified
+    if (s && slot_id[s] == slot_id[s - 1])
+      return fail(ctx, PSG_ERR_USAGE, "trace: request ids must be unique (id " +
+                                          std::to_string(slot_id[s]) + " repeats)");
   }
 
   // ---- units: (entry, replica), longest-first ----

@@ -113,3 +113,15 @@ def test_device_rank_keys_match_search_order(engine):
     perm = np.random.default_rng(0).permutation(len(keys))
     order = engine.rank_keys(keys[perm])
     assert list(keys[perm][order]["entry_index"]) == list(ranked.entries["entry_index"])
+
+
+def test_repeated_request_ids_are_rejected(engine):
+    """The reference keys per-request state by id (simulator.cpp:103-110); a
+    trace that repeats an id has no reproducible result, so the engine refuses
+    it loudly instead of guessing."""
+    from paper_2411_17651_b200.errors import UsageError
+    case = catalog.Case(fx.tiny_model(), catalog.ONE_DEV, fx.tiny_store([1, 100]),
+                        fx.trace_jsonl([(0, 10, 2, 0.0), (1, 10, 2, 0.0), (0, 12, 3, 0.1)]),
+                        plans=[(1, 1, catalog.TP1)])
+    with pytest.raises(UsageError, match="ids must be unique"):
+        case.gpu(engine)
