@@ -219,11 +219,19 @@ def main():
     from paper_2411_17651_b200.inputs import Config
     from paper_2411_17651_b200.workloads import WORKLOADS
 
+    # PSG_BENCH_BACKEND=gloo: a functional check of the multi-rank path on a
+    # box with fewer GPUs (ranks share devices, collectives on CPU tensors);
+    # never a measurement.
+    backend = os.environ.get("PSG_BENCH_BACKEND", "nccl")
+    dev = (local % max(1, torch.cuda.device_count())) if ws > 1 else 0
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local if ws > 1 else 0
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    coll_dev = dev if backend == "nccl" else "cpu"
     torch.cuda.set_device(dev)
     engine = Engine(dev)
     problems = [problem_for(WORKLOADS[k]) for k in keys]
@@ -264,7 +272,7 @@ def main():
                 st["best"].append(pdist.rank_keys_of(res, prob.plans.struct.enc_rank, objs[pi]))
         if ws > 1:  # one all_gather of ranking records per design space, ranked on device
             for keys_np in st["best"]:
-                engine.rank_keys(pdist.all_gather_keys(keys_np, device=dev))
+                engine.rank_keys(pdist.all_gather_keys(keys_np, device=dev if backend == "nccl" else None))
                 st["launches"] += 1
         st["wall_ms"] = 1e3 * (time.perf_counter() - t0)
         return st
@@ -289,7 +297,7 @@ def main():
         if ws == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
@@ -297,7 +305,7 @@ def main():
         if ws == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return t.item()
 
@@ -305,9 +313,11 @@ def main():
     wall_ms = [red_max(s["wall_ms"]) for s in steps]
     iters_step = red_sum(steps[0]["iters"])
     total_iters = iters_step * len(steps)
-    alg_bytes = sum(s["alg_bytes"] for s in steps)
-    sim_ms = sum(s["sim_ms"] for s in steps)
+    alg_bytes = red_sum(sum(s["alg_bytes"] for s in steps))
+    sim_ms = sum(red_max(s["sim_ms"]) for s in steps)
+    h2d_step, d2h_step = int(red_sum(steps[0]["h2d"])), int(red_sum(steps[0]["d2h"]))
     launches = int(red_sum(sum(s["launches"] for s in steps)))
+    entries_step = int(red_sum(steps[0]["entries"]))  # collectives: every rank, before rank 0 prints
     sims_per_step = len([k for k in keys])
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (sim_ms / 1e3) / 1e9
@@ -343,7 +353,7 @@ def main():
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": title, "design_spaces": keys,
-                   "entries_per_step": int(red_sum(steps[0]["entries"])),
+                   "entries_per_step": entries_step,
                    "plan_iterations_per_step": int(iters_step),
                    "requests": [int(p.trace.struct.n) for p in problems],
                    "l2": f"flushed between steps ({args.flush_mb} MB write)",
@@ -353,8 +363,8 @@ def main():
         "full_search_ms": {"device_median": statistics.median(dev_ms),
                            "e2e_median": statistics.median(wall_ms)},
         "e2e": {"value": total_iters / (sum(wall_ms) / 1e3), "unit": "plan-iter/s",
-                "h2d_bytes_per_step": int(steps[0]["h2d"]),
-                "d2h_bytes_per_step": int(steps[0]["d2h"])},
+                "h2d_bytes_per_step": h2d_step,
+                "d2h_bytes_per_step": d2h_step},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
