@@ -27,6 +27,8 @@ def main():
     ap.add_argument("keys", nargs="+")
     ap.add_argument("--top", type=int, default=5)
     ap.add_argument("--workdir", default="/tmp/psg_probe")
+    ap.add_argument("--native", action="store_true",
+                    help="build inputs with the native host library instead of the reference driver")
     args = ap.parse_args()
     os.environ.setdefault("PSG_LIBRARY", "libpsg_prof.so")
     for key in args.keys:
@@ -38,9 +40,23 @@ def run(key, args):
     out = os.path.join(args.workdir, f"phase_{args.key}.bin")
     os.makedirs(args.workdir, exist_ok=True)
     os.environ["PSG_PHASE_PROFILE"] = out
-    from harness import RefCase
     from paper_2411_17651_b200.engine import Engine
-    case = RefCase(args.key, args.workdir)
+    if args.native:
+        from paper_2411_17651_b200.host import problem_for
+        from paper_2411_17651_b200.inputs import Config
+        from paper_2411_17651_b200.workloads import WORKLOADS
+
+        class _Case:
+            pass
+        w = WORKLOADS[args.key]
+        prob = problem_for(w)
+        case = _Case()
+        case.plans, case.cluster, case.store, case.trace = prob.plans, prob.cluster, prob.store, prob.trace
+        case.workload = w
+        case.config = lambda: Config(objective=w.objective, freqs=w.freqs)
+    else:
+        from harness import RefCase
+        case = RefCase(args.key, args.workdir)
     eng = Engine(0)
     res = eng.search(case.plans, case.cluster, case.store, case.trace, case.config())
     raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 20)
