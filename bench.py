@@ -53,6 +53,8 @@ sys.path.insert(0, REPO)
 WORKLOAD_SETS = {
     "c2": (["c2", "c2fp8"], "C2: Llama-3-70B fp16+fp8 design spaces, 2x8 H100-sim cluster, "
                             "10k chat-lognormal requests, rate 8/s"),
+    "c2dvfs": (["c2dvfs", "c2fp8dvfs"], "C2 over the DVFS space: Llama-3-70B fp16+fp8 x "
+                                         "{0.8, 2.0} GHz, 2x8 H100-sim, 10k requests (supplementary)"),
     "c1": (["c1"], "C1: Llama-3-8B, 1x4 node, 1k requests 512/128"),
     "c3": (["c3"], "C3: GPT-3 175B, 4x8, 1188 summarization requests"),
     "c4": (["c4"], "C4: Mixtral 8x7B EP, 1x8, 512 creation requests, freqs {0.8,2.0}"),

@@ -161,6 +161,12 @@ WORKLOADS = {
     "c2fp8": Workload("c2fp8", "Llama-3-70B fp8, 2x8, 10k chat-lognormal, rate 8",
                       _fp8(LLAMA3_70B), cluster_json(2),
                       ("lognormal", (10000, 8.0, 2, [CHAT]))),
+    "c2dvfs": Workload("c2dvfs", "Llama-3-70B fp16, 2x8, 10k chat-lognormal, rate 8, DVFS {0.8,2.0}",
+                       LLAMA3_70B, cluster_json(2),
+                       ("lognormal", (10000, 8.0, 2, [CHAT])), freqs=[0.8, 2.0]),
+    "c2fp8dvfs": Workload("c2fp8dvfs", "Llama-3-70B fp8, 2x8, 10k chat-lognormal, rate 8, DVFS {0.8,2.0}",
+                          _fp8(LLAMA3_70B), cluster_json(2),
+                          ("lognormal", (10000, 8.0, 2, [CHAT])), freqs=[0.8, 2.0]),
     "c3": Workload("c3", "GPT-3 175B, 4x8, 1188 summarization req, rate 2",
                    GPT3_175B, cluster_json(4),
                    ("synth", SUMMARIZATION + (2.0, 1188, 7))),
