@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <new>
 #include <thread>
 #include <cstdlib>
 #include <cstring>
@@ -152,6 +153,21 @@ int fail(psg_context* ctx, int code, const std::string& msg) {
   return code;
 }
 
+// No C++ exception may cross the C ABI: host-side failures (allocation,
+// threads) become error codes with a message.
+template <typename F>
+int guarded(psg_context* ctx, F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, PSG_ERR_CUDA, "host memory allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, PSG_ERR_CUDA, std::string("host failure: ") + e.what());
+  } catch (...) {
+    return fail(ctx, PSG_ERR_CUDA, "host failure");
+  }
+}
+
 #define PSG_CUDA(call)                                                           \
   do {                                                                           \
     cudaError_t e_ = (call);                                                     \
@@ -163,7 +179,15 @@ int fail(psg_context* ctx, int code, const std::string& msg) {
 
 namespace psg {
 
+static int synth_compute_impl(psg_context* ctx, const psg_synth_grid* g, double* seconds,
+                              double* joules);
+
 int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, double* joules) {
+  return guarded(ctx, [&] { return synth_compute_impl(ctx, g, seconds, joules); });
+}
+
+static int synth_compute_impl(psg_context* ctx, const psg_synth_grid* g, double* seconds,
+                              double* joules) {
   if (!ctx || !g || !seconds || !joules) return PSG_ERR_USAGE;
   if (g->n_ctx < 1 || g->n_tasks < 1 || g->n_width < 1 || g->n_variants < 0)
     return fail(ctx, PSG_ERR_USAGE, "synth: empty grid axis");
@@ -200,8 +224,16 @@ int synth_compute(psg_context* ctx, const psg_synth_grid* g, double* seconds, do
   return PSG_OK;
 }
 
+static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
+                             int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
+
 int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
                  int32_t* phys, const int64_t* p2p_offset, int32_t* p2p) {
+  return guarded(ctx, [&] { return plan_compute_impl(ctx, s, records, phys, p2p_offset, p2p); });
+}
+
+static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
+                             int32_t* phys, const int64_t* p2p_offset, int32_t* p2p) {
   if (!ctx || !s || !records || !phys || !p2p_offset || !p2p) return PSG_ERR_USAGE;
   const int n = s->n_devices, G = s->n_groups, nc = s->n_cells;
   if (n < 1 || G < 0 || nc < 1 || nc > PSG_PLAN_MAX_CELLS || s->n_levels < 1)
@@ -287,7 +319,8 @@ int psg_context_create(int device, psg_context** out) {
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return PSG_ERR_CUDA;
   if (device < 0 || device >= count) return PSG_ERR_USAGE;
   if (cudaSetDevice(device) != cudaSuccess) return PSG_ERR_CUDA;
-  auto* ctx = new psg_context();
+  auto* ctx = new (std::nothrow) psg_context();
+  if (!ctx) return PSG_ERR_CUDA;
   ctx->device = device;
   {
     int v = 0;
@@ -355,9 +388,20 @@ int psg_rank_keys(psg_context* ctx, const psg_rank_key* keys, int64_t n, int64_t
   return PSG_OK;
 }
 
+static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
+                       const psg_store* S, const psg_trace* T, const psg_config* cfg,
+                       psg_result** out);
+
 int psg_search(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
                const psg_store* S, const psg_trace* T, const psg_config* cfg,
                psg_result** out) {
+  if (out) *out = nullptr;
+  return guarded(ctx, [&] { return search_impl(ctx, P, cl, S, T, cfg, out); });
+}
+
+static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluster* cl,
+                       const psg_store* S, const psg_trace* T, const psg_config* cfg,
+                       psg_result** out) {
   using clk = std::chrono::steady_clock;
   const auto t_start = clk::now();
   if (!ctx || !P || !cl || !S || !T || !cfg || !out) return PSG_ERR_USAGE;
@@ -1149,10 +1193,14 @@ int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* 
     rc[size_t(i)] = psg_search(ctxs[i], plans[i], clusters[i], stores[i], traces[i], configs[i], &outs[i]);
     ctxs[i]->concurrent_blocks = 0;
   };
-  std::vector<std::thread> pool;
-  for (int i = 1; i < n; ++i) pool.emplace_back(run, i);
-  run(0);
-  for (auto& t : pool) t.join();
+  const int spawn = guarded(ctxs[0], [&] {
+    std::vector<std::thread> pool;
+    for (int i = 1; i < n; ++i) pool.emplace_back(run, i);
+    run(0);
+    for (auto& t : pool) t.join();
+    return PSG_OK;
+  });
+  if (spawn != PSG_OK) return spawn;
   for (int i = 0; i < n; ++i)
     if (rc[size_t(i)] != PSG_OK) return rc[size_t(i)];
   if (kernel_span_ms) {
