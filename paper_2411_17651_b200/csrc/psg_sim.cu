@@ -77,6 +77,12 @@ struct CurveDesc {
 
 __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+#ifndef PSG_REG_ALL
+#define PSG_REG_ALL 0
+#endif
+#ifndef PSG_FILL_B
+#define PSG_FILL_B 32
+#endif
 constexpr int kMemoCap = 256;  // decode-cost memo entries (SimParams::memo_cap must match)
 
 // Fixed-size per-unit state lives in static shared memory: constant addresses,
@@ -288,6 +294,7 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
   return t;
 }
 
+
 }  // namespace
 
 // One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
@@ -479,6 +486,15 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated) <= cap_tok
   int64_t next_fin = kNoFin;
   int err = 0;
+  // Lane-resident mode: while the slots fit one warp (the common case), lane i
+  // holds slot i in registers and the slot arrays / finish summary are not
+  // maintained; spill() switches to the arrays when a 33rd slot is needed and
+  // fill() switches back once the batch is small again.
+  constexpr bool kReg = kSpec || PSG_REG_ALL;
+  bool regm = kReg;
+  int32_t r_tidx = 0, r_ctx = 0, r_gen = 0, r_done = 0, r_slot = 0;
+  int64_t r_fin = kDead;
+  double r_adm = 0.0, r_ft = 0.0, r_arr = 0.0;
   // extreme cell-query token counts and iteration totals (clamp reporting)
   int tok_lo = INT_MAX, tok_hi = -1;          // cell token counts (< 2^31)
   int64_t tot_lo = INT64_MAX, tot_hi = -1;     // iteration totals
@@ -604,8 +620,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     rebuild_summary();
   };
   auto migrate = [&]() {
-    // Move the active slots to the unit's global region: capacity n_req.
-    if (len > B) compact();
+    // Move the (compacted) active slots to the unit's global region: capacity n_req.
     __syncwarp();
     int32_t* gi = g_i + nr;
     int64_t* gfin = reinterpret_cast<int64_t*>(g_f + 3 * nr);
@@ -660,31 +675,117 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
     next_fin = abs_of(m);
   };
+  // lane-resident slots -> slot arrays + finish summary
+  auto spill = [&]() {
+    if (lane < len) {
+      a.tidx[lane] = r_tidx;
+      a.ctx[lane] = r_ctx;
+      a.gen[lane] = r_gen;
+      a.done[lane] = r_done;
+      a.slot[lane] = r_slot;
+      a.fin[lane] = r_fin;
+      a.adm[lane] = r_adm;
+      a.ft[lane] = r_ft;
+      a.arr[lane] = r_arr;
+    }
+    const unsigned pm = __ballot_sync(kFull, lane < len && r_fin == kNoFin);
+    first_pre = pm ? __ffs(pm) - 1 : len;
+    rebuild_summary();
+    regm = false;
+  };
+  // slot arrays -> lane-resident slots (len <= kWarp)
+  auto fill = [&]() {
+    __syncwarp();
+    r_fin = kDead;
+    if (lane < len) {
+      r_tidx = a.tidx[lane];
+      r_ctx = a.ctx[lane];
+      r_gen = a.gen[lane];
+      r_done = a.done[lane];
+      r_slot = a.slot[lane];
+      r_fin = a.fin[lane];
+      r_adm = a.adm[lane];
+      r_ft = a.ft[lane];
+      r_arr = a.arr[lane];
+    }
+    __syncwarp();
+    regm = kReg;
+  };
+  // order-preserving compaction of the lane-resident slots (staged through
+  // the otherwise unused slot arrays)
+  auto reg_compact = [&]() {
+    const bool live = lane < len && r_fin != kDead;
+    const unsigned km = __ballot_sync(kFull, live);
+    const int pos = __popc(km & lt_mask);
+    if (live) {
+      a.tidx[pos] = r_tidx;
+      a.ctx[pos] = r_ctx;
+      a.gen[pos] = r_gen;
+      a.done[pos] = r_done;
+      a.slot[pos] = r_slot;
+      a.fin[pos] = r_fin;
+      a.adm[pos] = r_adm;
+      a.ft[pos] = r_ft;
+      a.arr[pos] = r_arr;
+    }
+    len = __popc(km);
+    fill();
+  };
+  auto reg_trim = [&]() {
+    const unsigned lm = __ballot_sync(kFull, lane < len && r_fin != kDead);
+    len = lm ? kWarp - __clz(lm) : 0;
+  };
 
-  load_head();
+  // the queue head changed: reload it (the lane-resident variant keeps one
+  // call site of load_head for a smaller loop body)
+  bool head_dirty = kReg;
+  if (!kReg) load_head();
   while (true) {
     // ---- admit (batching.cpp:35-60) ----
     PROF_T0(t_adm);
-    while (hd_valid && hd_arr <= clock) {
+    while (true) {
+      if (kReg && head_dirty) {
+        load_head();
+        head_dirty = false;
+      }
+      if (!(hd_valid && hd_arr <= clock)) break;
       if (hd_ctx <= cap_tok) {  // context alone fits; else rejected below
         if (max_bs > 0 && int64_t(B) >= max_bs) break;
         if (used + hd_ctx > cap_tok) break;  // head blocks, FIFO
-        if (len >= cap_now) {
-          if (len > B) compact();
-          if (len >= cap_now) migrate();
+        if (regm && len == kWarp) {
+          if (B < kWarp) reg_compact();
+          if (len == kWarp) spill();
         }
-        if (lane == 0) {
-          if ((len & (kWarp - 1)) == 0) cm1[len / kWarp] = kNoFin;  // fresh chunk / group
-          if ((len & (kWarp * kWarp - 1)) == 0) cm2[len / (kWarp * kWarp)] = kNoFin;
-          a.tidx[len] = hd_tidx;
-          a.ctx[len] = hd_ctx;
-          a.gen[len] = hd_gen;
-          a.done[len] = 0;
-          a.slot[len] = hd_slot;
-          a.fin[len] = kNoFin;
-          a.adm[len] = clock;
-          a.ft[len] = 0.0;
-          a.arr[len] = hd_arr;
+        if (regm) {
+          if (lane == len) {
+            r_tidx = hd_tidx;
+            r_ctx = hd_ctx;
+            r_gen = hd_gen;
+            r_done = 0;
+            r_slot = hd_slot;
+            r_fin = kNoFin;
+            r_adm = clock;
+            r_ft = 0.0;
+            r_arr = hd_arr;
+          }
+        } else {
+          if (len >= cap_now) {
+            if (len > B) compact();
+            if (len >= cap_now) migrate();
+          }
+          if (lane == 0) {
+            if ((len & (kWarp - 1)) == 0) cm1[len / kWarp] = kNoFin;  // fresh chunk / group
+            if ((len & (kWarp * kWarp - 1)) == 0) cm2[len / (kWarp * kWarp)] = kNoFin;
+            a.tidx[len] = hd_tidx;
+            a.ctx[len] = hd_ctx;
+            a.gen[len] = hd_gen;
+            a.done[len] = 0;
+            a.slot[len] = hd_slot;
+            a.fin[len] = kNoFin;
+            a.adm[len] = clock;
+            a.ft[len] = 0.0;
+            a.arr[len] = hd_arr;
+          }
         }
         ++len;
         ++B;
@@ -695,7 +796,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         reject_slot(hd_slot);
       }
       if (hd_stack) --stack_top; else ++pend;
-      load_head();
+      if (kReg) head_dirty = true; else load_head();
     }
     __syncwarp();
     PROF_ADD(0, t_adm);
@@ -717,7 +818,22 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       int n_items = 0;
       int64_t pre_tok = 0;
       unsigned it_lo = 0xffffffffu, it_hi = 0;
-      for (int base = first_pre; base < len; base += kWarp) {
+      if (regm) {
+        const bool pre = lane < len && r_fin == kNoFin;
+        int tok = 0;
+        if (pre) {
+          int64_t t = int64_t(r_ctx) - r_done;
+          if (chunked) t = t < chunk ? t : chunk;
+          tok = int(t);
+        }
+        const unsigned pm = __ballot_sync(kFull, pre);
+        if (pre) a.items[__popc(pm & lt_mask)] = tok;
+        n_items = __popc(pm);
+        pre_tok = __reduce_add_sync(kFull, unsigned(tok));
+        it_lo = __reduce_min_sync(kFull, pre ? unsigned(tok) : 0xffffffffu);
+        it_hi = __reduce_max_sync(kFull, pre ? unsigned(tok) : 0u);
+      }
+      for (int base = regm ? len : first_pre; base < len; base += kWarp) {
         const int i = base + lane;
         const bool pre = i < len && a.fin[i] == kNoFin;
         int tok = 0;
@@ -817,7 +933,26 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       const int64_t n_new = n + 1;
       unsigned ncompl = 0, m = min_rel(next_fin, n_new);
       int new_fp = -1;
-      for (int base = first_pre & ~(kWarp - 1); base < len; base += kWarp) {  // whole chunks
+      if (regm) {
+        bool compl_now = false;
+        unsigned rel = kNoRel;
+        if (lane < len && r_fin == kNoFin) {
+          int64_t tok = int64_t(r_ctx) - r_done;
+          if (chunked) tok = tok < chunk ? tok : chunk;
+          const int64_t done = r_done + tok;
+          r_done = int32_t(done);
+          if (done == r_ctx) {  // the prefill iteration samples the first token
+            const int64_t fin = n_new + (r_gen > 1 ? r_gen - 1 : 0);
+            r_fin = fin;
+            r_ft = clock;
+            compl_now = true;
+            rel = unsigned(fin - n_new);
+          }
+        }
+        ncompl = __popc(__ballot_sync(kFull, compl_now));
+        m = min(m, __reduce_min_sync(kFull, rel));
+      }
+      for (int base = regm ? len : first_pre & ~(kWarp - 1); base < len; base += kWarp) {  // whole chunks
         const int i = base + lane;
         bool compl_now = false, still = false;
         unsigned rel = kNoRel;
@@ -931,7 +1066,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         const double c1 = __dadd_rn(clock, d);
         const double c2 = __dadd_rn(c1, d);
         const double c3 = __dadd_rn(c2, d);
-        if (!(clock < a_h && c1 < a_h && c2 < a_h && c3 < a_h)) break;
+        if (!(c3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
         clock = __dadd_rn(c3, d);
         energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
         flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
@@ -1006,7 +1141,29 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     // (simulator.cpp:143-156) at iteration n; finished slots become
     // tombstones ----
     PROF_T0(t_fin);
-    if (next_fin == n) {
+    if (next_fin == n && regm) {
+      PROF_CNT(13);
+      const bool fnow = lane < len && r_fin == n;
+      unsigned tok = 0;
+      if (fnow) {
+        const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? r_arr : r_adm;
+        const size_t s = slot_base + r_slot;
+        p.slot_e2e[s] = __dsub_rn(clock, r_arr);
+        p.slot_ttft[s] = __dsub_rn(r_ft, anchor);
+        p.slot_tpot[s] = __dsub_rn(clock, r_ft);  // / (gen - 1) in entry_reduce_kernel
+        p.slot_status[s] = 1;
+        r_fin = kDead;
+        tok = unsigned(r_ctx + r_gen);
+      }
+      const int64_t freed = int64_t(__reduce_add_sync(kFull, tok));
+      const int nfin = __popc(__ballot_sync(kFull, fnow));
+      const unsigned m = __reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel);
+      B -= nfin;
+      completed += nfin;
+      used -= freed;
+      next_fin = abs_of(m);
+      reg_trim();
+    } else if (next_fin == n) {
       PROF_CNT(13);
       int64_t freed = 0;
       unsigned m = kNoRel, nfin = 0;
@@ -1033,33 +1190,32 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         nfin += __popc(__ballot_sync(kFull, fnow));
         return __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n));
       };
-      if (nch == 1) {  // one chunk (small batches): no summary walk
+      if (!kReg && nch == 1) {  // one chunk (small batches): no summary walk
         m = finish_chunk(0);
         if (lane == 0) cm1[0] = cm2[0] = abs_of(m);
-      } else {
-        const int ng = (nch + kWarp - 1) / kWarp;
-        for (int gb = 0; gb < ng; gb += kWarp) {
-          const int g = gb + lane;
-          const int64_t v2 = g < ng ? cm2[g] : kNoFin;
-          unsigned gm = __ballot_sync(kFull, v2 == n);
-          m = min(m, __reduce_min_sync(kFull, v2 == n ? kNoRel : rel_of(v2)));
-          while (gm) {
-            const int grp = gb + __ffs(gm) - 1;
-            gm &= gm - 1;
-            const int c = grp * kWarp + lane;
-            int64_t v1 = c < nch ? cm1[c] : kNoFin;
-            unsigned cmask = __ballot_sync(kFull, v1 == n);
-            while (cmask) {
-              const int cl = __ffs(cmask) - 1;
-              cmask &= cmask - 1;
-              const unsigned cr = finish_chunk(grp * kWarp + cl);
-              if (lane == cl) v1 = abs_of(cr);
-              if (lane == 0) cm1[grp * kWarp + cl] = abs_of(cr);
-            }
-            const unsigned gr = __reduce_min_sync(kFull, rel_of(v1));
-            if (lane == 0) cm2[grp] = abs_of(gr);
-            m = min(m, gr);
+      }
+      const int ng = !kReg && nch == 1 ? 0 : (nch + kWarp - 1) / kWarp;
+      for (int gb = 0; gb < ng; gb += kWarp) {
+        const int g = gb + lane;
+        const int64_t v2 = g < ng ? cm2[g] : kNoFin;
+        unsigned gm = __ballot_sync(kFull, v2 == n);
+        m = min(m, __reduce_min_sync(kFull, v2 == n ? kNoRel : rel_of(v2)));
+        while (gm) {
+          const int grp = gb + __ffs(gm) - 1;
+          gm &= gm - 1;
+          const int c = grp * kWarp + lane;
+          int64_t v1 = c < nch ? cm1[c] : kNoFin;
+          unsigned cmask = __ballot_sync(kFull, v1 == n);
+          while (cmask) {
+            const int cl = __ffs(cmask) - 1;
+            cmask &= cmask - 1;
+            const unsigned cr = finish_chunk(grp * kWarp + cl);
+            if (lane == cl) v1 = abs_of(cr);
+            if (lane == 0) cm1[grp * kWarp + cl] = abs_of(cr);
           }
+          const unsigned gr = __reduce_min_sync(kFull, rel_of(v1));
+          if (lane == 0) cm2[grp] = abs_of(gr);
+          m = min(m, gr);
         }
       }
       __syncwarp();
@@ -1068,13 +1224,30 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       used -= freed;
       next_fin = abs_of(m);
       trim();
-      if (len > 2 * B + 2 * kWarp) compact();
+      const bool small = kReg && B <= PSG_FILL_B;  // small again: back to lane-resident slots
+      if (len > 2 * B + 2 * kWarp || (small && len > B)) compact();
+      if (small) fill();
     }
     PROF_ADD(7, t_fin);
     // ---- LIFO eviction on overflow (batching.cpp:110-125) ----
     PROF_T0(t_evi);
     bool evicted = false;
-    while (B > 1 && used > cap_tok) {
+    while (regm && B > 1 && used > cap_tok) {
+      const int i = len - 1;  // newest live request (trim invariant)
+      const int64_t fin = __shfl_sync(kFull, r_fin, i);
+      const int32_t gen = __shfl_sync(kFull, r_gen, i), ctx = __shfl_sync(kFull, r_ctx, i);
+      const int32_t tidx = __shfl_sync(kFull, r_tidx, i);
+      const int64_t tok = fin == kNoFin ? 0 : int64_t(gen) - (fin - n);
+      used -= int64_t(ctx) + tok;
+      if (fin == kNoFin) --n_pre;
+      if (lane == 0) g_stack[stack_top] = tidx;  // push_front of pending
+      if (lane == i) r_fin = kDead;
+      ++stack_top;
+      --B;
+      evicted = true;
+      reg_trim();
+    }
+    while (!regm && B > 1 && used > cap_tok) {
       const int i = len - 1;  // newest live request (trim invariant)
       const int64_t fin = a.fin[i];
       const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
@@ -1094,16 +1267,19 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       }
     }
     if (B == 1 && used > cap_tok) {  // a lone outgrowing request is rejected
-      reject_slot(a.slot[len - 1]);
+      reject_slot(regm ? __shfl_sync(kFull, r_slot, len - 1) : a.slot[len - 1]);
       B = len = first_pre = n_pre = 0;
       used = 0;
       next_fin = kNoFin;
-      evicted = false;
+      regm = kReg;  // empty: lane-resident
     }
     __syncwarp();
-    if (evicted) {
-      load_head();
-      recompute_next_fin();
+    if (evicted) {  // the evicted requests wait at the queue head (batching.cpp:114-118)
+      if (kReg) head_dirty = true; else load_head();
+      if (regm)
+        next_fin = abs_of(__reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel));
+      else
+        recompute_next_fin();
     }
     PROF_ADD(8, t_evi);
   }
