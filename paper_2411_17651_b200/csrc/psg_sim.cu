@@ -80,6 +80,9 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 #ifndef PSG_REG_ALL
 #define PSG_REG_ALL 0
 #endif
+#ifndef PSG_PIPE_MIN
+#define PSG_PIPE_MIN 8
+#endif
 #ifndef PSG_FILL_B
 #define PSG_FILL_B 32
 #endif
@@ -1062,6 +1065,27 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       const double a_h = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
       const int64_t ks = kmax < kSerial ? kmax : kSerial;
       int64_t j = 0;
+      if (ks >= PSG_PIPE_MIN) {
+        // software-pipelined by one group of 4: the arrival test of a group
+        // reads start clocks computed in the previous one, so the branch is
+        // off the clock's DADD dependency chain
+        double n1 = __dadd_rn(clock, d), n2 = __dadd_rn(n1, d), n3 = __dadd_rn(n2, d);
+        double n4 = __dadd_rn(n3, d);
+        while (j + 8 <= ks) {
+          if (!(n3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
+          const double m1 = __dadd_rn(n4, d), m2 = __dadd_rn(m1, d), m3 = __dadd_rn(m2, d);
+          const double m4 = __dadd_rn(m3, d);
+          clock = n4;
+          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+          j += 4;
+          n1 = m1;
+          n2 = m2;
+          n3 = m3;
+          n4 = m4;
+        }
+      }
       while (j + 4 <= ks) {
         const double c1 = __dadd_rn(clock, d);
         const double c2 = __dadd_rn(c1, d);
