@@ -48,7 +48,9 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 // slots: 0 admit, 1 mixed scan, 2 cost eval, 3 mixed advance, 4 decode cost,
 // 5 run setup, 6 tight loop, 7 finish, 8 evict, 9 head refill, 10 #mixed,
 // 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 #speculation hits, 15 total,
-// 16 cycles waited for speculation results, 17 eval cycles of misses.
+// 16 cycles waited for speculation results, 17 eval cycles of misses,
+// speculation misses by cause: 18 no job, 19 not one item, 20 other decode
+// count, 21 other tokens, 22 job not started.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -877,6 +879,13 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         const unsigned st = unsigned(__shfl_sync(kFull, vload(s_spec.started), 0));
         use_spec = st == spec_seq;
       }
+#ifdef PSG_PHASE_PROFILE
+      if (spec_on && !use_spec) {  // speculation miss: why
+        const int why = spec_tok < 0 ? 18 : n_items != 1 ? 19 : decode != spec_dec ? 20
+                        : a.items[0] != spec_tok ? 21 : 22;
+        prof_acc[why] += 1ull;
+      }
+#endif
       if (use_spec) {
         PROF_CNT(14);
         PROF_T0(t_wait);

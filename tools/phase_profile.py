@@ -19,7 +19,8 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 
 NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
          "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total",
-         "spec_wait_cyc", "miss_eval_cyc"]
+         "spec_wait_cyc", "miss_eval_cyc", "miss_nojob", "miss_items", "miss_decode", "miss_tok",
+         "miss_unstarted"]
 
 
 def main():
@@ -59,7 +60,7 @@ def run(key, args):
         case = RefCase(args.key, args.workdir)
     eng = Engine(0)
     res = eng.search(case.plans, case.cluster, case.store, case.trace, case.config())
-    raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 20)
+    raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 2 + len(NAMES))
     meta, cnt = raw[:, :2].view(np.int64), raw[:, 2:]
     if os.environ.get("PSG_CHAIN_REPLICAS", "1") != "0":
         # replicas of an entry run in order on one warp: aggregate per entry
@@ -84,6 +85,7 @@ def run(key, args):
         counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 15))
         hits, miss = max(1, int(cnt[u, 14])), max(1, int(cnt[u, 10]) - int(cnt[u, 14]))
         counts += f" | wait/hit={int(cnt[u, 16]) // hits} cyc, eval/miss={int(cnt[u, 17]) // miss} cyc"
+        counts += " | " + " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(18, len(NAMES)))
         print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
 
 
