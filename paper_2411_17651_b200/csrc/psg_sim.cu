@@ -79,6 +79,13 @@ struct CurveDesc {
 
 __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Compile-time tuning knobs (defaults are the measured best; A/B variants are
+// built with tools/variant_build.sh):
+//   PSG_REG_ALL   1: lane-resident slots in sim_kernel too (default: only the
+//                 speculation kernel)
+//   PSG_PIPE_MIN  shortest decode run stepped by the software-pipelined loop
+//   PSG_FILL_B    live slots at or below which a finish returns the batch to
+//                 lane-resident slots
 #ifndef PSG_REG_ALL
 #define PSG_REG_ALL 0
 #endif
