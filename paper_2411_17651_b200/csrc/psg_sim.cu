@@ -50,7 +50,8 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 // 11 #decode runs, 12 #decode table reads, 13 #finish events, 14 #speculation hits, 15 total,
 // 16 cycles waited for speculation results, 17 eval cycles of misses,
 // speculation misses by cause: 18 no job, 19 not one item, 20 other decode
-// count, 21 other tokens, 22 job not started.
+// count, 21 other tokens, 22 job not started; own evaluations: 23 query
+// values (loads + curves), 24 the four chains, 25 stage pass.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -152,7 +153,18 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
                                                   const int64_t total, const int64_t* cellq,
                                                   CurveDesc* cdesc, const double* tab,
                                                   const uint8_t* p2p_slot, double* qv,
-                                                  double* p2p_val) {
+                                                  double* p2p_val,
+                                                  unsigned long long* prof = nullptr) {
+#ifdef PSG_PHASE_PROFILE
+  long long pt = clock64();
+  auto pmark = [&](int slot) {
+    const long long t = clock64();
+    if (prof) prof[slot] += (unsigned long long)(t - pt);
+    pt = t;
+  };
+#else
+  auto pmark = [](int) {};
+#endif
   const int nq_c = n_items + (decode > 0 ? 1 : 0);
   const int Qc = E.C * nq_c;
   const int Q = Qc + E.NQ;
@@ -219,6 +231,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
       qv[3 * kQvStride + lane] = fb.y;
     }
     __syncwarp();
+    pmark(23);
     const int here = min(kWarp, Q - base);
     const int cell_end = min(here, max(0, Qc - base));
     const int coll_end = min(here, max(0, Qc + E.K - base));
@@ -230,6 +243,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
     }
     for (; l < end; ++l) chain = __dadd_rn(chain, qrow[l]);
     __syncwarp();
+    pmark(24);
   }
   const double bs = __shfl_sync(kFull, chain, 0);
   const double bj = __shfl_sync(kFull, chain, 1);
@@ -260,6 +274,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
   o.ce = ce;
   o.cf = __dmul_rn(__dmul_rn(__dmul_rn(bf, E.sdd), E.reps), E.Sd);
   o.cb = __dmul_rn(__dmul_rn(__dmul_rn(bb, E.sdd), E.reps), E.Sd);
+  pmark(25);
   return o;
 }
 
@@ -911,7 +926,11 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         PROF_T0(t_own);
         ev = eval_iteration(
             ectx, lane, [&](int i) { return a.items[i]; }, n_items, decode, total, cellq, cdesc,
-            tab, p2p_slot, qv, p2p_val);
+            tab, p2p_slot, qv, p2p_val
+#ifdef PSG_PHASE_PROFILE
+            , prof_acc
+#endif
+        );
         PROF_ADD(17, t_own);
       }
       const double srep = ev.srep, jrep = ev.jrep;

@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
          "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total",
          "spec_wait_cyc", "miss_eval_cyc", "miss_nojob", "miss_items", "miss_decode", "miss_tok",
-         "miss_unstarted"]
+         "miss_unstarted", "ev_query_cyc", "ev_chain_cyc", "ev_stage_cyc"]
 
 
 def main():
@@ -85,7 +85,9 @@ def run(key, args):
         counts = " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(10, 15))
         hits, miss = max(1, int(cnt[u, 14])), max(1, int(cnt[u, 10]) - int(cnt[u, 14]))
         counts += f" | wait/hit={int(cnt[u, 16]) // hits} cyc, eval/miss={int(cnt[u, 17]) // miss} cyc"
-        counts += " | " + " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(18, len(NAMES)))
+        counts += " | " + " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(18, 23))
+        own = max(1, int(cnt[u, 10]) - int(cnt[u, 14]))
+        counts += " | per own eval: " + " ".join(f"{NAMES[k]}={int(cnt[u, k]) // own}" for k in range(23, 26))
         print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
 
 
