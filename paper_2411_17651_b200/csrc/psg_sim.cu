@@ -1034,13 +1034,18 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       // ---- decode-only run: exact macro-stepping ----
       PROF_CNT(11);
       PROF_T0(t_d1);
-      double d, e, f, b;
-      if (B <= kMemoCap && memo[4 * (B - 1)] >= 0.0) {
-        d = memo[4 * (B - 1)];
-        e = memo[4 * (B - 1) + 1];
-        f = memo[4 * (B - 1) + 2];
-        b = memo[4 * (B - 1) + 3];
-      } else {
+      // decode-only cost of B: the memo row (two 16-byte loads issued
+      // together), else the entry's decode table (first run at this B)
+      double d = -1.0, e = 0.0, f = 0.0, b = 0.0;
+      if (B <= kMemoCap) {
+        const double2* mrow = reinterpret_cast<const double2*>(memo + 4 * (B - 1));
+        const double2 de = mrow[0], fb = mrow[1];
+        d = de.x;
+        e = de.y;
+        f = fb.x;
+        b = fb.y;
+      }
+      if (!(d >= 0.0)) {
         PROF_CNT(12);
         const double2* row = reinterpret_cast<const double2*>(dtab + int64_t(B - 1) * 4);
         const double2 de = __ldg(row), fb = __ldg(row + 1);
@@ -1057,9 +1062,11 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
           }
           __syncwarp();
         }
+        // decode-run batch extremes for the clamp report: every batch size
+        // passes here on its first run
+        run_lo = min(run_lo, B);
+        run_hi = max(run_hi, B);
       }
-      run_lo = min(run_lo, B);
-      run_hi = max(run_hi, B);
       PROF_ADD(4, t_d1);
       PROF_T0(t_d2);
       // iterations until the first finish (inclusive), cut at the first KV
