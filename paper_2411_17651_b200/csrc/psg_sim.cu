@@ -1297,55 +1297,57 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     PROF_ADD(7, t_fin);
     // ---- LIFO eviction on overflow (batching.cpp:110-125) ----
     PROF_T0(t_evi);
-    bool evicted = false;
-    while (regm && B > 1 && used > cap_tok) {
-      const int i = len - 1;  // newest live request (trim invariant)
-      const int64_t fin = __shfl_sync(kFull, r_fin, i);
-      const int32_t gen = __shfl_sync(kFull, r_gen, i), ctx = __shfl_sync(kFull, r_ctx, i);
-      const int32_t tidx = __shfl_sync(kFull, r_tidx, i);
-      const int64_t tok = fin == kNoFin ? 0 : int64_t(gen) - (fin - n);
-      used -= int64_t(ctx) + tok;
-      if (fin == kNoFin) --n_pre;
-      if (lane == 0) g_stack[stack_top] = tidx;  // push_front of pending
-      if (lane == i) r_fin = kDead;
-      ++stack_top;
-      --B;
-      evicted = true;
-      reg_trim();
-    }
-    while (!regm && B > 1 && used > cap_tok) {
-      const int i = len - 1;  // newest live request (trim invariant)
-      const int64_t fin = a.fin[i];
-      const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
-      used -= int64_t(a.ctx[i]) + tok;
-      if (fin == kNoFin) --n_pre;
-      if (lane == 0) {
-        g_stack[stack_top] = a.tidx[i];  // push_front of pending
-        a.fin[i] = kDead;
+    if (used > cap_tok) {  // KV overflow (rare): the block below
+      bool evicted = false;
+      while (regm && B > 1 && used > cap_tok) {
+        const int i = len - 1;  // newest live request (trim invariant)
+        const int64_t fin = __shfl_sync(kFull, r_fin, i);
+        const int32_t gen = __shfl_sync(kFull, r_gen, i), ctx = __shfl_sync(kFull, r_ctx, i);
+        const int32_t tidx = __shfl_sync(kFull, r_tidx, i);
+        const int64_t tok = fin == kNoFin ? 0 : int64_t(gen) - (fin - n);
+        used -= int64_t(ctx) + tok;
+        if (fin == kNoFin) --n_pre;
+        if (lane == 0) g_stack[stack_top] = tidx;  // push_front of pending
+        if (lane == i) r_fin = kDead;
+        ++stack_top;
+        --B;
+        evicted = true;
+        reg_trim();
       }
-      ++stack_top;
-      --B;
-      evicted = true;
-      trim();
-      if (fin != kNoFin) {  // a decode slot left the summary
-        fix_chunk(i / kWarp);
-        fix_group(i / (kWarp * kWarp));
+      while (!regm && B > 1 && used > cap_tok) {
+        const int i = len - 1;  // newest live request (trim invariant)
+        const int64_t fin = a.fin[i];
+        const int64_t tok = fin == kNoFin ? 0 : int64_t(a.gen[i]) - (fin - n);
+        used -= int64_t(a.ctx[i]) + tok;
+        if (fin == kNoFin) --n_pre;
+        if (lane == 0) {
+          g_stack[stack_top] = a.tidx[i];  // push_front of pending
+          a.fin[i] = kDead;
+        }
+        ++stack_top;
+        --B;
+        evicted = true;
+        trim();
+        if (fin != kNoFin) {  // a decode slot left the summary
+          fix_chunk(i / kWarp);
+          fix_group(i / (kWarp * kWarp));
+        }
       }
-    }
-    if (B == 1 && used > cap_tok) {  // a lone outgrowing request is rejected
-      reject_slot(regm ? __shfl_sync(kFull, r_slot, len - 1) : a.slot[len - 1]);
-      B = len = first_pre = n_pre = 0;
-      used = 0;
-      next_fin = kNoFin;
-      regm = kReg;  // empty: lane-resident
-    }
-    __syncwarp();
-    if (evicted) {  // the evicted requests wait at the queue head (batching.cpp:114-118)
-      if (kReg) head_dirty = true; else load_head();
-      if (regm)
-        next_fin = abs_of(__reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel));
-      else
-        recompute_next_fin();
+      if (B == 1 && used > cap_tok) {  // a lone outgrowing request is rejected
+        reject_slot(regm ? __shfl_sync(kFull, r_slot, len - 1) : a.slot[len - 1]);
+        B = len = first_pre = n_pre = 0;
+        used = 0;
+        next_fin = kNoFin;
+        regm = kReg;  // empty: lane-resident
+      }
+      __syncwarp();
+      if (evicted) {  // the evicted requests wait at the queue head (batching.cpp:114-118)
+        if (kReg) head_dirty = true; else load_head();
+        if (regm)
+          next_fin = abs_of(__reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel));
+        else
+          recompute_next_fin();
+      }
     }
     PROF_ADD(8, t_evi);
   }
