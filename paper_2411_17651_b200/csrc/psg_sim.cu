@@ -1207,92 +1207,94 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     // (simulator.cpp:143-156) at iteration n; finished slots become
     // tombstones ----
     PROF_T0(t_fin);
-    if (next_fin == n && regm) {
-      PROF_CNT(13);
-      const bool fnow = lane < len && r_fin == n;
-      unsigned tok = 0;
-      if (fnow) {
-        const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? r_arr : r_adm;
-        const size_t s = slot_base + r_slot;
-        p.slot_e2e[s] = __dsub_rn(clock, r_arr);
-        p.slot_ttft[s] = __dsub_rn(r_ft, anchor);
-        p.slot_tpot[s] = __dsub_rn(clock, r_ft);  // / (gen - 1) in entry_reduce_kernel
-        p.slot_status[s] = 1;
-        r_fin = kDead;
-        tok = unsigned(r_ctx + r_gen);
-      }
-      const int64_t freed = int64_t(__reduce_add_sync(kFull, tok));
-      const int nfin = __popc(__ballot_sync(kFull, fnow));
-      const unsigned m = __reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel);
-      B -= nfin;
-      completed += nfin;
-      used -= freed;
-      next_fin = abs_of(m);
-      reg_trim();
-    } else if (next_fin == n) {
-      PROF_CNT(13);
-      int64_t freed = 0;
-      unsigned m = kNoRel, nfin = 0;
-      const int nch = (len + kWarp - 1) / kWarp;
-      // finishes of chunk ch (metrics, tombstones); returns its new min rel fin
-      auto finish_chunk = [&](int ch) -> unsigned {
-        const int i = ch * kWarp + lane;
-        const int64_t fin = i < len ? a.fin[i] : kDead;
-        const bool fnow = fin == n;
+    if (next_fin == n) {  // finishes at this iteration
+      if (regm) {
+        PROF_CNT(13);
+        const bool fnow = lane < len && r_fin == n;
         unsigned tok = 0;
         if (fnow) {
-          const int32_t gen = a.gen[i];
-          const double arr = a.arr[i], ft = a.ft[i];
-          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
-          const size_t s = slot_base + a.slot[i];
-          p.slot_e2e[s] = __dsub_rn(clock, arr);
-          p.slot_ttft[s] = __dsub_rn(ft, anchor);
-          p.slot_tpot[s] = __dsub_rn(clock, ft);  // / (gen - 1) in entry_reduce_kernel
+          const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? r_arr : r_adm;
+          const size_t s = slot_base + r_slot;
+          p.slot_e2e[s] = __dsub_rn(clock, r_arr);
+          p.slot_ttft[s] = __dsub_rn(r_ft, anchor);
+          p.slot_tpot[s] = __dsub_rn(clock, r_ft);  // / (gen - 1) in entry_reduce_kernel
           p.slot_status[s] = 1;
-          a.fin[i] = kDead;
-          tok = unsigned(a.ctx[i] + gen);
+          r_fin = kDead;
+          tok = unsigned(r_ctx + r_gen);
         }
-        freed += int64_t(__reduce_add_sync(kFull, tok));
-        nfin += __popc(__ballot_sync(kFull, fnow));
-        return __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n));
-      };
-      if (!kReg && nch == 1) {  // one chunk (small batches): no summary walk
-        m = finish_chunk(0);
-        if (lane == 0) cm1[0] = cm2[0] = abs_of(m);
-      }
-      const int ng = !kReg && nch == 1 ? 0 : (nch + kWarp - 1) / kWarp;
-      for (int gb = 0; gb < ng; gb += kWarp) {
-        const int g = gb + lane;
-        const int64_t v2 = g < ng ? cm2[g] : kNoFin;
-        unsigned gm = __ballot_sync(kFull, v2 == n);
-        m = min(m, __reduce_min_sync(kFull, v2 == n ? kNoRel : rel_of(v2)));
-        while (gm) {
-          const int grp = gb + __ffs(gm) - 1;
-          gm &= gm - 1;
-          const int c = grp * kWarp + lane;
-          int64_t v1 = c < nch ? cm1[c] : kNoFin;
-          unsigned cmask = __ballot_sync(kFull, v1 == n);
-          while (cmask) {
-            const int cl = __ffs(cmask) - 1;
-            cmask &= cmask - 1;
-            const unsigned cr = finish_chunk(grp * kWarp + cl);
-            if (lane == cl) v1 = abs_of(cr);
-            if (lane == 0) cm1[grp * kWarp + cl] = abs_of(cr);
+        const int64_t freed = int64_t(__reduce_add_sync(kFull, tok));
+        const int nfin = __popc(__ballot_sync(kFull, fnow));
+        const unsigned m = __reduce_min_sync(kFull, lane < len ? min_rel(r_fin, n) : kNoRel);
+        B -= nfin;
+        completed += nfin;
+        used -= freed;
+        next_fin = abs_of(m);
+        reg_trim();
+      } else {
+        PROF_CNT(13);
+        int64_t freed = 0;
+        unsigned m = kNoRel, nfin = 0;
+        const int nch = (len + kWarp - 1) / kWarp;
+        // finishes of chunk ch (metrics, tombstones); returns its new min rel fin
+        auto finish_chunk = [&](int ch) -> unsigned {
+          const int i = ch * kWarp + lane;
+          const int64_t fin = i < len ? a.fin[i] : kDead;
+          const bool fnow = fin == n;
+          unsigned tok = 0;
+          if (fnow) {
+            const int32_t gen = a.gen[i];
+            const double arr = a.arr[i], ft = a.ft[i];
+            const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
+            const size_t s = slot_base + a.slot[i];
+            p.slot_e2e[s] = __dsub_rn(clock, arr);
+            p.slot_ttft[s] = __dsub_rn(ft, anchor);
+            p.slot_tpot[s] = __dsub_rn(clock, ft);  // / (gen - 1) in entry_reduce_kernel
+            p.slot_status[s] = 1;
+            a.fin[i] = kDead;
+            tok = unsigned(a.ctx[i] + gen);
           }
-          const unsigned gr = __reduce_min_sync(kFull, rel_of(v1));
-          if (lane == 0) cm2[grp] = abs_of(gr);
-          m = min(m, gr);
+          freed += int64_t(__reduce_add_sync(kFull, tok));
+          nfin += __popc(__ballot_sync(kFull, fnow));
+          return __reduce_min_sync(kFull, fnow ? kNoRel : min_rel(fin, n));
+        };
+        if (!kReg && nch == 1) {  // one chunk (small batches): no summary walk
+          m = finish_chunk(0);
+          if (lane == 0) cm1[0] = cm2[0] = abs_of(m);
         }
+        const int ng = !kReg && nch == 1 ? 0 : (nch + kWarp - 1) / kWarp;
+        for (int gb = 0; gb < ng; gb += kWarp) {
+          const int g = gb + lane;
+          const int64_t v2 = g < ng ? cm2[g] : kNoFin;
+          unsigned gm = __ballot_sync(kFull, v2 == n);
+          m = min(m, __reduce_min_sync(kFull, v2 == n ? kNoRel : rel_of(v2)));
+          while (gm) {
+            const int grp = gb + __ffs(gm) - 1;
+            gm &= gm - 1;
+            const int c = grp * kWarp + lane;
+            int64_t v1 = c < nch ? cm1[c] : kNoFin;
+            unsigned cmask = __ballot_sync(kFull, v1 == n);
+            while (cmask) {
+              const int cl = __ffs(cmask) - 1;
+              cmask &= cmask - 1;
+              const unsigned cr = finish_chunk(grp * kWarp + cl);
+              if (lane == cl) v1 = abs_of(cr);
+              if (lane == 0) cm1[grp * kWarp + cl] = abs_of(cr);
+            }
+            const unsigned gr = __reduce_min_sync(kFull, rel_of(v1));
+            if (lane == 0) cm2[grp] = abs_of(gr);
+            m = min(m, gr);
+          }
+        }
+        __syncwarp();
+        B -= int(nfin);
+        completed += nfin;
+        used -= freed;
+        next_fin = abs_of(m);
+        trim();
+        const bool small = kReg && B <= PSG_FILL_B;  // small again: back to lane-resident slots
+        if (len > 2 * B + 2 * kWarp || (small && len > B)) compact();
+        if (small) fill();
       }
-      __syncwarp();
-      B -= int(nfin);
-      completed += nfin;
-      used -= freed;
-      next_fin = abs_of(m);
-      trim();
-      const bool small = kReg && B <= PSG_FILL_B;  // small again: back to lane-resident slots
-      if (len > 2 * B + 2 * kWarp || (small && len > B)) compact();
-      if (small) fill();
     }
     PROF_ADD(7, t_fin);
     // ---- LIFO eviction on overflow (batching.cpp:110-125) ----
