@@ -859,8 +859,8 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         pre_tok = __reduce_add_sync(kFull, unsigned(tok));
         it_lo = __reduce_min_sync(kFull, pre ? unsigned(tok) : 0xffffffffu);
         it_hi = __reduce_max_sync(kFull, pre ? unsigned(tok) : 0u);
-      }
-      for (int base = regm ? len : first_pre; base < len; base += kWarp) {
+      } else {
+      for (int base = first_pre; base < len; base += kWarp) {
         const int i = base + lane;
         const bool pre = i < len && a.fin[i] == kNoFin;
         int tok = 0;
@@ -875,6 +875,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         pre_tok += __reduce_add_sync(kFull, unsigned(tok));
         it_lo = min(it_lo, __reduce_min_sync(kFull, pre ? unsigned(tok) : 0xffffffffu));
         it_hi = max(it_hi, __reduce_max_sync(kFull, pre ? unsigned(tok) : 0u));
+      }
       }
       __syncwarp();
       const int64_t decode = int64_t(B) - n_items;
@@ -989,8 +990,8 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         }
         ncompl = __popc(__ballot_sync(kFull, compl_now));
         m = min(m, __reduce_min_sync(kFull, rel));
-      }
-      for (int base = regm ? len : first_pre & ~(kWarp - 1); base < len; base += kWarp) {  // whole chunks
+      } else {
+      for (int base = first_pre & ~(kWarp - 1); base < len; base += kWarp) {  // whole chunks
         const int i = base + lane;
         bool compl_now = false, still = false;
         unsigned rel = kNoRel;
@@ -1023,8 +1024,9 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         const unsigned sm = __ballot_sync(kFull, still);
         if (new_fp < 0 && sm) new_fp = base + __ffs(sm) - 1;
       }
-      __syncwarp();
       first_pre = new_fp < 0 ? len : new_fp;
+      }
+      __syncwarp();
       used += decode + int64_t(ncompl);
       n_pre -= int(ncompl);
       n = n_new;
