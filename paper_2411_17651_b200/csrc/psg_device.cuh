@@ -90,7 +90,7 @@ struct SimParams {
   int32_t anchor;
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
-  int32_t serial_run;        // decode-run iterations stepped serially before the closed form
+  int32_t serial_run;        // decode runs longer than this take the closed form
   int32_t chain_replicas;    // 1: grid = entries, replicas run in order with one tally
   int32_t speculate;         // 1: blockDim 64, a second warp prices the next mixed iteration
   int32_t spec_sleep_ns;     // the speculation warp's polling interval

@@ -103,6 +103,37 @@ PSG_HD bool segment(double acc, double inc, Segment& g) {
   return true;
 }
 
+// The mantissa-independent part of segment(): for acc's binade (exponent
+// field eb, normal positive acc) and inc, the per-step increment R and
+// whether s = inc / ulp is a tie (then R holds only from an even mantissa).
+// Cacheable per (inc, eb).  Returns false where segment() never applies.
+PSG_HD bool segment_key(double acc, double inc, int64_t& eb, int64_t& R, bool& tie) {
+  const int64_t b = bits_of(acc);
+  eb = (b >> 52) & 0x7ff;
+  if (b < 0 || eb == 0 || eb == 0x7ff) return false;
+  tie = false;
+  if (inc == 0.0 && bits_of(inc) == 0) {  // +0: every addition leaves acc as it is
+    R = 0;
+    return true;
+  }
+  const int64_t ib = bits_of(inc);
+  const int64_t ie = (ib >> 52) & 0x7ff;
+  if (ib <= 0 || ie == 0 || ie == 0x7ff) return false;
+  const int64_t shift = 1075 - eb;
+  if (ie + shift >= 1023 + 52) return false;
+  if (ie + shift < 1023 - 2) {
+    R = 0;
+    return true;
+  }
+  const double s = of_bits(ib + shift * kHidden);
+  const double fl = floor(s);
+  const double frac = s - fl;
+  const int64_t R0 = int64_t(fl);
+  tie = frac == 0.5;
+  R = tie ? R0 + (R0 & 1) : int64_t(frac > 0.5 ? fl + 1.0 : fl);
+  return true;
+}
+
 PSG_HD double compose(int64_t m, int64_t ebits) {
   return of_bits((ebits << 52) | (m - kHidden));
 }

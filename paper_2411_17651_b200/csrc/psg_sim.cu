@@ -108,6 +108,9 @@ __shared__ __align__(16) double s_p2p_val[2 * kMaxClampSlots];    // p2p (second
 __shared__ __align__(16) double s_w_arr[kWindow];                 // prefetch window: arrival
 __shared__ __align__(16) int32_t s_w_i32[4 * kWindow];            // tidx, ctx, gen, slot
 __shared__ __align__(16) double s_memo[4 * kMemoCap];             // decode-only cost per B
+// closed-form decode runs: per (B, accumulator) the binade segment key
+// (exponent field << 53 | tie << 52 | R; 0 = none), psg_fastsum.cuh segment_key
+__shared__ __align__(16) unsigned long long s_rkey[4 * kMemoCap];
 
 struct SmemLayout {
   size_t qv, cdesc, cellq, p2p_slot, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
@@ -389,7 +392,10 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   uint64_t p2p_mask = 0;  // ND <= 2: bit b = distinct-curve slot of boundary b
   __syncwarp();
   for (int b = 0; b < NB && ND <= 2; ++b) p2p_mask |= uint64_t(p2p_slot[b]) << b;
-  for (int i = lane; i < 4 * kMemoCap; i += kWarp) memo[i] = -1.0;
+  for (int i = lane; i < 4 * kMemoCap; i += kWarp) {
+    memo[i] = -1.0;
+    s_rkey[i] = 0ull;
+  }
   if (lane < C) {
     const int sig = p.cell_sig[size_t(U.fslot) * p.n_cells_total + c0 + lane];
     cellq[lane] = p.qoff[sig];
@@ -1101,100 +1107,116 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       bool stop = false;
       PROF_ADD(5, t_d2);
       PROF_T0(t_d3);
-      // k sequential additions in closed form (psg_fastsum.cuh), bit-exact
-      // Short runs step serially (a dependent DADD per iteration); a run
-      // still going after kSerial iterations finishes in closed form
-      // (psg_fastsum.cuh), bit-exact either way.
-      const int64_t kSerial = p.serial_run;
-      const double a_h = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
-      const int64_t ks = kmax < kSerial ? kmax : kSerial;
       int64_t j = 0;
-      if (ks >= PSG_PIPE_MIN) {
-        // software-pipelined by one group of 4: the arrival test of a group
-        // reads start clocks computed in the previous one, so the branch is
-        // off the clock's DADD dependency chain
-        double n1 = __dadd_rn(clock, d), n2 = __dadd_rn(n1, d), n3 = __dadd_rn(n2, d);
-        double n4 = __dadd_rn(n3, d);
-        while (j + 8 <= ks) {
-          if (!(n3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
-          const double m1 = __dadd_rn(n4, d), m2 = __dadd_rn(m1, d), m3 = __dadd_rn(m2, d);
-          const double m4 = __dadd_rn(m3, d);
-          clock = n4;
-          energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-          flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-          bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-          j += 4;
-          n1 = m1;
-          n2 = m2;
-          n3 = m3;
-          n4 = m4;
+      bool cf = false;
+      if (kmax > p.serial_run) {
+        // Closed-form run (psg_fastsum.cuh): lanes 1..3 carry energy / flops /
+        // bytes, the others the clock.  Each accumulator's binade segment
+        // (per-step mantissa increment R) depends only on its increment —
+        // fixed for this B — and its exponent, so it is cached per (B,
+        // accumulator) and the whole run is integer arithmetic when every
+        // accumulator's segment is cached and the run stays in its binade.
+        const int al = (lane >= 1 && lane <= 3) ? lane : 0;
+        const double acc = al == 1 ? energy : al == 2 ? flops : al == 3 ? bytes : clock;
+        const double inc = al == 1 ? e : al == 2 ? f : al == 3 ? b : d;
+        const uint64_t abits = uint64_t(__double_as_longlong(acc));
+        unsigned long long key = B <= kMemoCap ? s_rkey[4 * (B - 1) + al] : 0ull;
+        if ((key >> 53) != (abits >> 52)) {  // new batch size or binade: derive it
+          int64_t keb = 0, R = 0;
+          bool tie = false;
+          key = 0ull;
+          if (fastsum::segment_key(acc, inc, keb, R, tie) && R < (int64_t(1) << 52))
+            key = (uint64_t(keb) << 53) | (uint64_t(tie) << 52) | uint64_t(R);
+          if (B <= kMemoCap && lane < 4) s_rkey[4 * (B - 1) + lane] = key;
         }
-      }
-      while (j + 4 <= ks) {
-        const double c1 = __dadd_rn(clock, d);
-        const double c2 = __dadd_rn(c1, d);
-        const double c3 = __dadd_rn(c2, d);
-        if (!(c3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
-        clock = __dadd_rn(c3, d);
-        energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-        flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-        bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-        j += 4;
-      }
-      while (j < ks && clock < a_h) {
-        clock = __dadd_rn(clock, d);
-        energy = __dadd_rn(energy, e);
-        flops = __dadd_rn(flops, f);
-        bytes = __dadd_rn(bytes, b);
-        ++j;
-      }
-      if (j == ks && j < kmax) {
-        const int64_t j0 = j;
-        if (check) j += fastsum::advance_until(clock, d, kmax - j, a_h);
-        int64_t rest = 0;  // clock additions left after the arrival check
-        if (j < kmax && !(check && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok))) {
-          rest = kmax - j;
-          j = kmax;
-        }
-        // lanes 0..3 advance clock (rest), energy, flops, bytes (j - j0 each)
-        const double acc = lane == 0 ? clock : lane == 1 ? energy : lane == 2 ? flops : bytes;
-        const double inc = lane == 0 ? d : lane == 1 ? e : lane == 2 ? f : b;
-        const int64_t kk = lane == 0 ? rest : (lane < 4 ? j - j0 : 0);
-        const double r = fastsum::add_n(acc, inc, kk);
-        clock = __shfl_sync(kFull, r, 0);
-        energy = __shfl_sync(kFull, r, 1);
-        flops = __shfl_sync(kFull, r, 2);
-        bytes = __shfl_sync(kFull, r, 3);
-      }
-      if (j < kmax && check && (rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) {
-        stop = true;
-      } else if (j < kmax) {
-        // the arrived head cannot join this run: finish it (serial part only
-        // reaches here with j < kSerial)
-        const int64_t k2 = kmax - j;
-        if (k2 <= kSerial) {
-          for (; j + 4 <= kmax; j += 4) {
-            clock = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(clock, d), d), d), d);
-            energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
-            flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
-            bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+        const int64_t m = int64_t(abits & uint64_t(fastsum::kHidden - 1)) | fastsum::kHidden;
+        const int64_t R = int64_t(key & ((uint64_t(1) << 52) - 1));
+        const bool ok = key != 0ull && !(((key >> 52) & 1) && (m & 1)) &&
+                        (R == 0 || fastsum::fits(kmax, R, fastsum::kTop - 2 - m));
+        if (__all_sync(kFull, ok)) {
+          const int64_t Rc = __shfl_sync(kFull, R, 0);  // the clock's segment
+          const int64_t mc = __shfl_sync(kFull, m, 0);
+          const int64_t ec = int64_t(__double_as_longlong(clock) >> 52);
+          double a = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
+          while (true) {
+            int64_t t = kmax - j;  // iterations from j whose start clock is below a
+            if (j == 0 && check) {
+              if (!(clock < a)) {
+                t = 0;
+              } else if (Rc > 0) {
+                const int64_t ab = __double_as_longlong(a);
+                if ((ab >> 52) == ec) {  // a in the clock's binade: a = M * ulp
+                  const int64_t gap = ((ab & (fastsum::kHidden - 1)) | fastsum::kHidden) - mc;
+                  const int64_t ta = fastsum::floor_div(gap - 1, Rc) + 1;
+                  t = ta < t ? ta : t;
+                }  // else a lies above the binade: every step starts below it
+              }
+            }
+            j += t;
+            if (j < kmax && !(rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) continue;
+            break;
           }
-          for (; j < kmax; ++j) {
-            clock = __dadd_rn(clock, d);
-            energy = __dadd_rn(energy, e);
-            flops = __dadd_rn(flops, f);
-            bytes = __dadd_rn(bytes, b);
-          }
-        } else {
-          const double acc = lane == 0 ? clock : lane == 1 ? energy : lane == 2 ? flops : bytes;
-          const double inc = lane == 0 ? d : lane == 1 ? e : lane == 2 ? f : b;
-          const double r = fastsum::add_n(acc, inc, lane < 4 ? k2 : 0);
+          const double r = R > 0 ? fastsum::compose(m + j * R, int64_t(abits >> 52)) : acc;
           clock = __shfl_sync(kFull, r, 0);
           energy = __shfl_sync(kFull, r, 1);
           flops = __shfl_sync(kFull, r, 2);
           bytes = __shfl_sync(kFull, r, 3);
-          j = kmax;
+          stop = j < kmax;
+          cf = true;
         }
+      }
+      if (!cf) {
+        // serial stepping (short runs, and runs the closed form cannot take:
+        // a binade crossing, a tie from an odd mantissa)
+        double a_h = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
+        while (true) {
+          if (kmax - j >= PSG_PIPE_MIN) {
+            // software-pipelined by one group of 4: the arrival test of a group
+            // reads start clocks computed in the previous one, so the branch is
+            // off the clock's DADD dependency chain
+            double n1 = __dadd_rn(clock, d), n2 = __dadd_rn(n1, d), n3 = __dadd_rn(n2, d);
+            double n4 = __dadd_rn(n3, d);
+            while (j + 8 <= kmax) {
+              if (!(n3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
+              const double m1 = __dadd_rn(n4, d), m2 = __dadd_rn(m1, d), m3 = __dadd_rn(m2, d);
+              const double m4 = __dadd_rn(m3, d);
+              clock = n4;
+              energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+              flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+              bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+              j += 4;
+              n1 = m1;
+              n2 = m2;
+              n3 = m3;
+              n4 = m4;
+            }
+          }
+          while (j + 4 <= kmax) {
+            const double c1 = __dadd_rn(clock, d);
+            const double c2 = __dadd_rn(c1, d);
+            const double c3 = __dadd_rn(c2, d);
+            if (!(c3 < a_h)) break;
+            clock = __dadd_rn(c3, d);
+            energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
+            flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
+            bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
+            j += 4;
+          }
+          while (j < kmax && clock < a_h) {
+            clock = __dadd_rn(clock, d);
+            energy = __dadd_rn(energy, e);
+            flops = __dadd_rn(flops, f);
+            bytes = __dadd_rn(bytes, b);
+            ++j;
+          }
+          // the head arrived at iteration j; one that cannot join lets the run go on
+          if (j < kmax && !(rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) {
+            a_h = __longlong_as_double(0x7ff0000000000000ll);
+            continue;
+          }
+          break;
+        }
+        stop = j < kmax;
       }
       PROF_ADD(6, t_d3);
       n += j;
