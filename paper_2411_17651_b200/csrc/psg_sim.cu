@@ -223,28 +223,24 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
       if (k >= E.K) {
         p2p_val[k - E.K] = sec;
         p2p_val[kMaxClampSlots + k - E.K] = en;
+      } else {
+        te = make_double2(sec, en);  // a collective adds seconds and energy only
       }
-      qv[lane] = sec;
-      qv[kQvStride + lane] = en;
     }
-    if (cell_lane) {
-      qv[lane] = te.x;
-      qv[kQvStride + lane] = __dmul_rn(te.y, E.sdd);  // query_energy * stage_devices
-      qv[2 * kQvStride + lane] = fb.x;
-      qv[3 * kQvStride + lane] = fb.y;
-    }
+    // Every lane writes its column — p2p and idle lanes zeros — so the four
+    // chains run one uniform, 4-aligned trip count: the accumulators are sums
+    // of non-negative values starting at +0, where adding +0.0 is exact.
+    qv[lane] = te.x;
+    qv[kQvStride + lane] = cell_lane ? __dmul_rn(te.y, E.sdd) : te.y;  // cells: x stage_devices
+    qv[2 * kQvStride + lane] = fb.x;
+    qv[3 * kQvStride + lane] = fb.y;
     __syncwarp();
     pmark(23);
-    const int here = min(kWarp, Q - base);
-    const int cell_end = min(here, max(0, Qc - base));
-    const int coll_end = min(here, max(0, Qc + E.K - base));
-    const int end = lane < 2 ? coll_end : (lane < 4 ? cell_end : 0);
-    int l = 0;
-    for (; l + 4 <= end; l += 4) {
+    const int coll_end = min(kWarp, max(0, Qc + E.K - base));
+    for (int l = 0; l < coll_end; l += 4) {
       const double v0 = qrow[l], v1 = qrow[l + 1], v2 = qrow[l + 2], v3 = qrow[l + 3];
       chain = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(chain, v0), v1), v2), v3);
     }
-    for (; l < end; ++l) chain = __dadd_rn(chain, qrow[l]);
     __syncwarp();
     pmark(24);
   }
