@@ -142,7 +142,9 @@ struct psg_context {
 namespace {
 
 void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
-  if (sp.speculate)
+  if (sp.emit_it)
+    sim_kernel_emit<<<blocks, kWarp, smem, st>>>(sp);
+  else if (sp.speculate)
     sim_kernel_spec<<<blocks, 2 * kWarp, smem, st>>>(sp);
   else
     sim_kernel<<<blocks, kWarp, smem, st>>>(sp);
@@ -336,12 +338,12 @@ int psg_context_create(int device, psg_context** out) {
   }
   // the cap only; each launch asks for what it needs (set once: contexts may
   // launch concurrently from several threads)
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec}) {
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit}) {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, k) == cudaSuccess)
       ctx->sim_static_smem = std::max<int64_t>(ctx->sim_static_smem, int64_t(fa.sharedSizeBytes));
   }
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec})
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(ctx->smem_block_max - ctx->sim_static_smem));
   for (auto& e : ctx->ev) cudaEventCreate(&e);

@@ -325,7 +325,7 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 
 // One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
 // carry WorkTally across the entry's replicas (simulator.cpp:195-201).
-template <bool kSpec>
+template <bool kSpec, bool kEmit>
 __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
                                          double& tally_flops, double& tally_bytes,
                                          unsigned char* smem_raw) {
@@ -364,7 +364,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
 
   // the speculation warp reads the unit's staged state: let it go idle first
-  const bool spec_on = kSpec && !p.emit_it && p.speculate == 1;  // 2: helper idles (dev)
+  const bool spec_on = kSpec && !kEmit && p.speculate == 1;  // 2: helper idles (dev)
   if (spec_on)
     while (unsigned(vload(s_spec.done)) != unsigned(vload64(s_spec.job) >> 44)) {
     }
@@ -502,7 +502,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const bool chunked = p.batch_mode == PSG_BATCH_CHUNKED;
   const int64_t chunk = p.chunk_size;
   const int64_t max_bs = p.entry_max_bs ? p.entry_max_bs[U.entry] : p.max_batch_size;
-  const bool stepwise = p.emit_it != nullptr;  // iteration records: no macro-stepping
+  constexpr bool stepwise = kEmit;  // iteration records (second pass): no macro-stepping
   const bool chunk_err = chunked && chunk < 1;
   const bool missing = p.entry_missing[U.entry] != 0;
 
@@ -1470,7 +1470,7 @@ __device__ __noinline__ void spec_helper(const double* tab, const unsigned sleep
 }
 
 // One warp per entry (or unit); with kSpec a second warp per block speculates.
-template <bool kSpec>
+template <bool kSpec, bool kEmit>
 __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
   double tf = 0.0, tb = 0.0;
   // chained: one warp per entry runs its replicas in order with one running
@@ -1480,7 +1480,7 @@ __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* sme
   const int k0 = p.chain_replicas ? p.entry_unit_begin[e] : e;
   const int k1 = p.chain_replicas ? p.entry_unit_begin[e + 1] : e + 1;
   for (int k = k0; k < k1; ++k) {
-    sim_unit<kSpec>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
+    sim_unit<kSpec, kEmit>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
     __syncwarp();
   }
 }
@@ -1500,13 +1500,20 @@ __global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) {
                 unsigned(p.spec_sleep_ns));
     return;
   }
-  sim_block<true>(p, smem_raw);
+  sim_block<true, false>(p, smem_raw);
   if (threadIdx.x == 0) vstore(s_spec.quit, 1);
 }
 
 __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  sim_block<false>(p, smem_raw);
+  sim_block<false, false>(p, smem_raw);
+}
+
+// The iteration-record pass (psg_config::emit_iterations): every iteration
+// stepped and recorded, no speculation.
+__global__ void __launch_bounds__(32, 8) sim_kernel_emit(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sim_block<false, true>(p, smem_raw);
 }
 
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {
