@@ -142,12 +142,13 @@ struct psg_context {
 namespace {
 
 void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
+  const bool chunked = sp.batch_mode == PSG_BATCH_CHUNKED;
   if (sp.emit_it)
     sim_kernel_emit<<<blocks, kWarp, smem, st>>>(sp);
   else if (sp.speculate)
-    sim_kernel_spec<<<blocks, 2 * kWarp, smem, st>>>(sp);
+    (chunked ? sim_kernel_spec_chunked : sim_kernel_spec)<<<blocks, 2 * kWarp, smem, st>>>(sp);
   else
-    sim_kernel<<<blocks, kWarp, smem, st>>>(sp);
+    (chunked ? sim_kernel_chunked : sim_kernel)<<<blocks, kWarp, smem, st>>>(sp);
 }
 
 int fail(psg_context* ctx, int code, const std::string& msg) {
@@ -338,12 +339,14 @@ int psg_context_create(int device, psg_context** out) {
   }
   // the cap only; each launch asks for what it needs (set once: contexts may
   // launch concurrently from several threads)
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit}) {
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+                        (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked}) {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, k) == cudaSuccess)
       ctx->sim_static_smem = std::max<int64_t>(ctx->sim_static_smem, int64_t(fa.sharedSizeBytes));
   }
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit})
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+                        (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(ctx->smem_block_max - ctx->sim_static_smem));
   for (auto& e : ctx->ev) cudaEventCreate(&e);

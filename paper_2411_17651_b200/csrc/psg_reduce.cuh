@@ -50,6 +50,8 @@ int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* rec
 __global__ void sim_kernel(const SimParams p);       // one warp per block
 __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per block
 __global__ void sim_kernel_emit(const SimParams p);  // iteration-record pass
+__global__ void sim_kernel_chunked(const SimParams p);       // chunked-prefill variants
+__global__ void sim_kernel_spec_chunked(const SimParams p);
 __global__ void entry_reduce_kernel(const ReduceParams r);
 __global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
                                int64_t* rj_off, int64_t* totals);

@@ -325,7 +325,9 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 
 // One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
 // carry WorkTally across the entry's replicas (simulator.cpp:195-201).
-template <bool kSpec, bool kEmit>
+// kMode: batching mode fixed at compile time (1 contiguous, 2 chunked) or
+// read from the parameters (0).
+template <bool kSpec, bool kEmit, int kMode>
 __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
                                          double& tally_flops, double& tally_bytes,
                                          unsigned char* smem_raw) {
@@ -499,7 +501,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
                    : int(int64_t(U.replica) + int64_t(j) * U.replicas);
   };
   const size_t slot_base = size_t(U.entry) * size_t(p.n_slots);
-  const bool chunked = p.batch_mode == PSG_BATCH_CHUNKED;
+  const bool chunked = kMode == 2 || (kMode == 0 && p.batch_mode == PSG_BATCH_CHUNKED);
   const int64_t chunk = p.chunk_size;
   const int64_t max_bs = p.entry_max_bs ? p.entry_max_bs[U.entry] : p.max_batch_size;
   constexpr bool stepwise = kEmit;  // iteration records (second pass): no macro-stepping
@@ -1470,7 +1472,7 @@ __device__ __noinline__ void spec_helper(const double* tab, const unsigned sleep
 }
 
 // One warp per entry (or unit); with kSpec a second warp per block speculates.
-template <bool kSpec, bool kEmit>
+template <bool kSpec, bool kEmit, int kMode>
 __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
   double tf = 0.0, tb = 0.0;
   // chained: one warp per entry runs its replicas in order with one running
@@ -1480,12 +1482,13 @@ __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* sme
   const int k0 = p.chain_replicas ? p.entry_unit_begin[e] : e;
   const int k1 = p.chain_replicas ? p.entry_unit_begin[e + 1] : e + 1;
   for (int k = k0; k < k1; ++k) {
-    sim_unit<kSpec, kEmit>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
+    sim_unit<kSpec, kEmit, kMode>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
     __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) {
+template <int kMode>
+__device__ __forceinline__ void spec_block(const SimParams& p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (threadIdx.x == 0) {
     s_spec.job = 0;
@@ -1500,20 +1503,28 @@ __global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) {
                 unsigned(p.spec_sleep_ns));
     return;
   }
-  sim_block<true, false>(p, smem_raw);
+  sim_block<true, false, kMode>(p, smem_raw);
   if (threadIdx.x == 0) vstore(s_spec.quit, 1);
 }
 
+__global__ void __launch_bounds__(64, 4) sim_kernel_spec(const SimParams p) { spec_block<1>(p); }
+__global__ void __launch_bounds__(64, 4) sim_kernel_spec_chunked(const SimParams p) { spec_block<2>(p); }
+
 __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  sim_block<false, false>(p, smem_raw);
+  sim_block<false, false, 1>(p, smem_raw);
+}
+
+__global__ void __launch_bounds__(32, 8) sim_kernel_chunked(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sim_block<false, false, 2>(p, smem_raw);
 }
 
 // The iteration-record pass (psg_config::emit_iterations): every iteration
 // stepped and recorded, no speculation.
 __global__ void __launch_bounds__(32, 8) sim_kernel_emit(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  sim_block<false, true>(p, smem_raw);
+  sim_block<false, true, 0>(p, smem_raw);
 }
 
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap) {
