@@ -1006,7 +1006,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     }
   }
   PSG_CUDA(cudaEventRecord(ctx->ev[2], st));
-  entry_reduce_kernel<<<E, 256, 0, st>>>(rp);
+  entry_reduce_kernel<<<E, kReduceThreads, 0, st>>>(rp);
   offsets_kernel<<<1, 32, 0, st>>>(rp.eout, E, (int64_t*)W(w_proff), (int64_t*)W(w_rjoff),
                                    (int64_t*)W(w_tot));
   launches += 2;

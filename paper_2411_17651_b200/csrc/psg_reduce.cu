@@ -37,7 +37,7 @@ __device__ __forceinline__ int64_t nearest_rank(double q, int64_t n) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) entry_reduce_kernel(const ReduceParams r) {
+__global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const ReduceParams r) {
   const int e = blockIdx.x;
   __shared__ unsigned sel_hist[5][256];
   __shared__ uint64_t sel_prefix[5];

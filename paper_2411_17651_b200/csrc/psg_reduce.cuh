@@ -52,6 +52,9 @@ __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per
 __global__ void sim_kernel_emit(const SimParams p);  // iteration-record pass
 __global__ void sim_kernel_chunked(const SimParams p);       // chunked-prefill variants
 __global__ void sim_kernel_spec_chunked(const SimParams p);
+// One CTA per entry; 32 warps hide the slot arrays' load latency in the
+// radix-select sweeps.
+constexpr int kReduceThreads = 1024;
 __global__ void entry_reduce_kernel(const ReduceParams r);
 __global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
                                int64_t* rj_off, int64_t* totals);
