@@ -256,19 +256,37 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
   }
 }
 
-// Exclusive scan of per-entry completed / rejected counts (single CTA).
+// Exclusive scan of per-entry completed / rejected counts (one warp, 32
+// entries per step: shuffle scan, running totals carried across steps).
 __global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
                                int64_t* rj_off, int64_t* totals) {
-  if (threadIdx.x != 0) return;
-  int64_t a = 0, b = 0;
-  for (int e = 0; e < n_entries; ++e) {
-    pr_off[e] = a;
-    rj_off[e] = b;
-    a += eout[e].completed;
-    b += eout[e].rejected;
+  const int lane = threadIdx.x;
+  if (lane >= 32) return;
+  int64_t a = 0, b = 0;  // totals of the entries before this step
+  for (int e0 = 0; e0 < n_entries; e0 += 32) {
+    const int e = e0 + lane;
+    const int64_t ca = e < n_entries ? eout[e].completed : 0;
+    const int64_t cb = e < n_entries ? eout[e].rejected : 0;
+    int64_t ia = ca, ib = cb;  // inclusive scans
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t ya = __shfl_up_sync(0xffffffffu, ia, off);
+      const int64_t yb = __shfl_up_sync(0xffffffffu, ib, off);
+      if (lane >= off) {
+        ia += ya;
+        ib += yb;
+      }
+    }
+    if (e < n_entries) {
+      pr_off[e] = a + ia - ca;
+      rj_off[e] = b + ib - cb;
+    }
+    a += __shfl_sync(0xffffffffu, ia, 31);
+    b += __shfl_sync(0xffffffffu, ib, 31);
   }
-  totals[0] = a;
-  totals[1] = b;
+  if (lane == 0) {
+    totals[0] = a;
+    totals[1] = b;
+  }
 }
 
 // Dense per_request / rejected_ids in ascending id order per entry.
