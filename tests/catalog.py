@@ -162,6 +162,33 @@ def random_batching(seed):
                 fx.trace_jsonl(reqs), plans=[(1, 1, TP1)], **cfg)
 
 
+def random_batching_wide(seed):
+    """Seeded traces whose batches repeatedly grow past one warp (32 slots)
+    and shrink again, so the speculation kernel's lane-resident slots spill to
+    the slot arrays, come back and compact lazily, under KV pressure (LIFO
+    eviction, re-admission, rejection), chunked prefill and batch caps."""
+    rng = random.Random(10_000 + seed)
+    n = 60 + rng.randrange(90)
+    grow = seed % 2 == 1  # short prompts, long generations: decode growth overflows the ledger
+    t, reqs = 0.0, []
+    for i in range(n):
+        t += rng.randrange(3) * 0.0005
+        ctx = 1 + rng.randrange(8 if grow else 60)
+        gen = (20 + rng.randrange(60)) if grow else 1 + rng.randrange(60)
+        reqs.append((i, ctx, gen, t))
+    mem = (3000.0 + 200.0 * rng.randrange(200)) if grow else 20000.0 + 400.0 * rng.randrange(250)
+    cfg = {}
+    if rng.randrange(4) == 0:
+        cfg["max_batch_size"] = 33 + rng.randrange(40)
+    if rng.randrange(3) == 0:
+        cfg["batching"] = "chunked"
+        cfg["chunk_size"] = 1 + rng.randrange(48)
+    if rng.randrange(4) == 0:
+        cfg["ttft_anchor"] = "admission"
+    return Case(fx.tiny_model(), tiny_budget_cluster(mem), fx.tiny_store([1, 4, 16, 100, 1024]),
+                fx.trace_jsonl(reqs), plans=[(1, 1, TP1)], **cfg)
+
+
 NAMED = {
     "single_request": single_request, "empty_trace": empty_trace,
     "pipeline_two_stages": pipeline_two_stages, "dp2_full": dp2_full, "dp1_half": dp1_half,

@@ -32,6 +32,20 @@ def test_engine_matches_oracle_on_random_batching(engine, seed):
     assert e["num_completed"] + e["num_rejected"] == len(case.prob.trace)
 
 
+@pytest.mark.parametrize("spec", ["1", "0"])
+@pytest.mark.parametrize("seed", range(40))
+def test_engine_matches_oracle_on_wide_batches(engine, monkeypatch, seed, spec):
+    """Batches crossing 32 slots both ways: the speculation kernel's
+    lane-resident slots (spill / fill / lazy compaction) and the plain
+    kernel's slot arrays give the oracle's results."""
+    monkeypatch.setenv("PSG_SPECULATE", spec)
+    case = catalog.random_batching_wide(seed)
+    g = case.gpu(engine)
+    same_results(g, case.oracle())
+    e = g.entries[0]
+    assert e["num_completed"] + e["num_rejected"] == len(case.prob.trace)
+
+
 def test_known_answers_on_device(engine):
     e = catalog.single_request().gpu(engine).entries[0]
     assert abs(e["e2e_latency"] - 0.0303) <= 1e-12 * 0.0303
