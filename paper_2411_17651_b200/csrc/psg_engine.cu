@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <new>
@@ -122,7 +124,24 @@ const char* dtype_name(int d) {
 
 }  // namespace
 
+// Start gate of concurrent searches (psg_search_many): every search enqueues
+// its inputs, then all launch their kernels together, so the device span is
+// not stretched by one search's host-side preparation.  A search that fails
+// before the gate still arrives (on exit), so the others never wait for it.
+struct StartGate {
+  std::mutex m;
+  std::condition_variable cv;
+  int expected = 0, arrived = 0;
+  void arrive(bool wait) {
+    std::unique_lock<std::mutex> lk(m);
+    if (++arrived >= expected) cv.notify_all();
+    if (wait) cv.wait(lk, [&] { return arrived >= expected; });
+  }
+};
+
 struct psg_context {
+  StartGate* gate = nullptr;       // psg_search_many: launch together
+  bool gate_passed = false;
   int device = 0;
   int n_sm = 148;                  // device properties used to size the simulation launch
   int64_t smem_sm = 228 * 1024, smem_block_max = 227 * 1024;
@@ -950,6 +969,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   PSG_CUDA(cudaMemsetAsync(sp.slot_status, 0, std::max<size_t>(slots, 1), st));
   PSG_CUDA(cudaMemsetAsync(W(w_cc), 0, wk.size - w_cc, st));
   PSG_CUDA(cudaEventRecord(ctx->ev[1], st));
+  if (ctx->gate && !ctx->gate_passed) {
+    ctx->gate_passed = true;
+    ctx->gate->arrive(true);
+  }
   const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem, sp.cm2_cap);
   if (prof_path) std::fprintf(stderr, "psg: units=%d smem_cap=%d smem=%zu B\n", n_units, sp.smem_cap, smem);
   if (n_sig > 0) {  // cell-query tables, then decode-only iteration tables
@@ -1193,9 +1216,16 @@ int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* 
                                    : plans[i]->n_plans * std::max(1, c->n_freqs);
   }
   std::vector<int> rc(size_t(n), PSG_OK);
+  StartGate gate;
+  gate.expected = n;
+  const bool gated = !std::getenv("PSG_NO_START_GATE");  // dev knob
   auto run = [&](int i) {
     ctxs[i]->concurrent_blocks = total;
+    ctxs[i]->gate = gated ? &gate : nullptr;
+    ctxs[i]->gate_passed = false;
     rc[size_t(i)] = psg_search(ctxs[i], plans[i], clusters[i], stores[i], traces[i], configs[i], &outs[i]);
+    if (gated && !ctxs[i]->gate_passed) gate.arrive(false);  // failed before the gate
+    ctxs[i]->gate = nullptr;
     ctxs[i]->concurrent_blocks = 0;
   };
   const int spawn = guarded(ctxs[0], [&] {
