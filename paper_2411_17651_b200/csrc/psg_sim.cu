@@ -16,7 +16,9 @@
 //  * Shared memory holds everything an event touches: the active slots
 //    (SoA, tombstoned, migrating to a global region only if the batch
 //    outgrows them), a 32-request prefetch window of the replica's arrivals,
-//    a decode-cost memo, and the unit's collective curves.
+//    a decode-cost memo with the cached binade segments, and the unit's
+//    collective curves.  In the speculation kernel a batch of at most one
+//    warp lives in registers instead (lane i = slot i).
 //  * The KV ledger is an exact integer: cap_tok = max{T : double(T)*kv <= cap}
 //    turns every admission / overflow / admissibility test into an integer
 //    compare.
@@ -24,7 +26,8 @@
 //    {decode_count = B}, so its (seconds, joules, flops, bytes) are bit-
 //    identical until the batch changes.  Between events (arrival of an
 //    admissible/rejectable head, first finish, first KV overflow) the unit
-//    runs a tight loop of the reference's sequential FP64 adds only.
+//    runs the reference's sequential FP64 adds (software-pipelined), or for
+//    long runs their exact closed form (psg_fastsum.cuh).
 //  * Clamp warnings (cost.cpp:204-212, :273-278) are monotone in the token
 //    count, so the unit tracks the extreme token counts / totals it queried
 //    and derives the per-table flags once at the end.
