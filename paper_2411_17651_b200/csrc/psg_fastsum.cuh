@@ -16,7 +16,11 @@
 //   tie from an odd m, zero/negative/subnormal operands and non-finite values
 //   fall back to one plain addition.
 //
-// Host and device share this code so the CPU test
+// The simulation kernel caches segment_key() — R and the tie flag depend only
+// on the increment and acc's exponent — per (batch size, accumulator) and
+// runs a decode run as compose(m + t*R) with the arrival step from
+// floor_div(); add_n() / advance_until() are the general multi-binade forms
+// (tests, tools).  Host and device share this code so the CPU test
 // (tests/test_cpu_fastsum.py) checks it against sequential stepping.
 #pragma once
 #include <math.h>
