@@ -328,6 +328,32 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 
 // One DP replica (run_replica, simulator.cpp:98-172).  tally_flops / _bytes
 // carry WorkTally across the entry's replicas (simulator.cpp:195-201).
+// Refills the 32-request prefetch window from request w_base (rare: once per
+// 32 admissions; out of line so the admit path stays compact).
+__device__ __noinline__ void refill_window(const int32_t* seq, const double* arrival,
+                                           const int64_t* ctx, const int64_t* gen,
+                                           const int32_t* slot, int64_t seq_base, int replica,
+                                           int replicas, int n_req, int w_base, bool chunked,
+                                           int64_t chunk, int C, const double* qtab,
+                                           const int64_t* cellq) {
+  const int lane = threadIdx.x & (kWarp - 1);
+  const int j = w_base + lane;
+  if (j < n_req) {
+    const int t = seq ? seq[seq_base + j] : int(int64_t(replica) + int64_t(j) * replicas);
+    s_w_arr[lane] = arrival[t];
+    s_w_i32[lane] = t;
+    s_w_i32[kWindow + lane] = int(ctx[t]);
+    s_w_i32[2 * kWindow + lane] = int(gen[t]);
+    s_w_i32[3 * kWindow + lane] = slot[t];
+    // warm L1 with the cell rows this request's prefill will read
+    int64_t first = ctx[t];
+    if (chunked && chunk >= 1 && first > chunk) first = chunk;
+    for (int c = 0; c < C; ++c)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(qtab + (cellq[c] + first) * 4));
+  }
+  __syncwarp();
+}
+
 // kMode: batching mode fixed at compile time (1 contiguous, 2 chunked) or
 // read from the parameters (0).
 template <bool kSpec, bool kEmit, int kMode>
@@ -554,21 +580,26 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     if (pend >= w_base + kWindow) {  // refill the prefetch window
       PROF_T0(t_ref);
       w_base = pend;
-      const int j = w_base + lane;
-      if (j < U.n_req) {
-        const int t = req_tidx(j);
-        w_arr[lane] = p.T.arrival[t];
-        w_i32[lane] = t;
-        w_i32[kWindow + lane] = int(p.T.ctx[t]);
-        w_i32[2 * kWindow + lane] = int(p.T.gen[t]);
-        w_i32[3 * kWindow + lane] = p.T.slot[t];
-        // warm L1 with the cell rows this request's prefill will read
-        int64_t first = p.T.ctx[t];
-        if (chunked && chunk >= 1 && first > chunk) first = chunk;
-        for (int c = 0; c < C; ++c)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(qtab + (cellq[c] + first) * 4));
+      if (kSpec) {  // out of line: the speculation kernel's admit path stays compact
+        refill_window(p.T.seq, p.T.arrival, p.T.ctx, p.T.gen, p.T.slot, U.seq_base, U.replica,
+                      U.replicas, U.n_req, w_base, chunked, chunk, C, qtab, cellq);
+      } else {
+        const int j = w_base + lane;
+        if (j < U.n_req) {
+          const int t = req_tidx(j);
+          w_arr[lane] = p.T.arrival[t];
+          w_i32[lane] = t;
+          w_i32[kWindow + lane] = int(p.T.ctx[t]);
+          w_i32[2 * kWindow + lane] = int(p.T.gen[t]);
+          w_i32[3 * kWindow + lane] = p.T.slot[t];
+          // warm L1 with the cell rows this request's prefill will read
+          int64_t first = p.T.ctx[t];
+          if (chunked && chunk >= 1 && first > chunk) first = chunk;
+          for (int c = 0; c < C; ++c)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(qtab + (cellq[c] + first) * 4));
+        }
+        __syncwarp();
       }
-      __syncwarp();
       PROF_ADD(9, t_ref);
     }
     const int w = pend - w_base;
