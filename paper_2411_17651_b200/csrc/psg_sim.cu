@@ -1201,14 +1201,17 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         // serial stepping (short runs, and runs the closed form cannot take:
         // a binade crossing, a tie from an odd mantissa)
         double a_h = check ? hd_arr : __longlong_as_double(0x7ff0000000000000ll);
+        // 32-bit counters: a run is bounded by one request's remaining decode steps
+        const int km = int(kmax);
+        int jj = 0;
         while (true) {
-          if (kmax - j >= PSG_PIPE_MIN) {
+          if (km - jj >= PSG_PIPE_MIN) {
             // software-pipelined by one group of 4: the arrival test of a group
             // reads start clocks computed in the previous one, so the branch is
             // off the clock's DADD dependency chain
             double n1 = __dadd_rn(clock, d), n2 = __dadd_rn(n1, d), n3 = __dadd_rn(n2, d);
             double n4 = __dadd_rn(n3, d);
-            while (j + 8 <= kmax) {
+            while (jj + 8 <= km) {
               if (!(n3 < a_h)) break;  // start clocks never decrease (d >= 0 or NaN)
               const double m1 = __dadd_rn(n4, d), m2 = __dadd_rn(m1, d), m3 = __dadd_rn(m2, d);
               const double m4 = __dadd_rn(m3, d);
@@ -1216,14 +1219,14 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
               energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
               flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
               bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-              j += 4;
+              jj += 4;
               n1 = m1;
               n2 = m2;
               n3 = m3;
               n4 = m4;
             }
           }
-          while (j + 4 <= kmax) {
+          while (jj + 4 <= km) {
             const double c1 = __dadd_rn(clock, d);
             const double c2 = __dadd_rn(c1, d);
             const double c3 = __dadd_rn(c2, d);
@@ -1232,22 +1235,23 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
             energy = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(energy, e), e), e), e);
             flops = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(flops, f), f), f), f);
             bytes = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(bytes, b), b), b), b);
-            j += 4;
+            jj += 4;
           }
-          while (j < kmax && clock < a_h) {
+          while (jj < km && clock < a_h) {
             clock = __dadd_rn(clock, d);
             energy = __dadd_rn(energy, e);
             flops = __dadd_rn(flops, f);
             bytes = __dadd_rn(bytes, b);
-            ++j;
+            ++jj;
           }
           // the head arrived at iteration j; one that cannot join lets the run go on
-          if (j < kmax && !(rej_h || used + j * int64_t(B) + hd_ctx <= cap_tok)) {
+          if (jj < km && !(rej_h || used + int64_t(jj) * B + hd_ctx <= cap_tok)) {
             a_h = __longlong_as_double(0x7ff0000000000000ll);
             continue;
           }
           break;
         }
+        j = jj;
         stop = j < kmax;
       }
       PROF_ADD(6, t_d3);
