@@ -296,6 +296,9 @@ struct SimConfig {
   BatchPolicy policy;
   TtftAnchor ttft_anchor = TtftAnchor::Arrival;
   bool emit_iterations = false;  // simulate_plan only (simulator.hpp:77)
+  // TTFT-SLO-constrained ranking (psg.h psg_config.ttft_slo; not in the
+  // reference): > 0 ranks entries whose slo_quantile TTFT meets it first
+  double ttft_slo = 0.0, slo_quantile = 0.0;
 };
 
 // plansim::IterationRecord (simulator.hpp:35-42).
@@ -320,6 +323,8 @@ struct SimulationReport {
   int64_t num_completed = 0, num_rejected = 0, num_iterations = 0, max_batch_observed = 0;
   // additive outputs (not in the reference)
   double p50_ttft = 0.0, p99_ttft = 0.0, p50_tpot = 0.0, p99_tpot = 0.0;
+  double slo_ttft = 0.0;  // TTFT at SimConfig::slo_quantile (ttft_slo > 0)
+  bool slo_met = false;
   std::vector<RequestMetrics> per_request;
   std::vector<int64_t> rejected_ids;
   std::vector<IterationRecord> iterations;  // emit_iterations

@@ -176,6 +176,15 @@ typedef struct psg_config {
   /* SimConfig::emit_iterations (simulator.hpp:77): one IterationRecord per
      iteration (simulator.cpp:158-170); requires exactly one entry */
   int32_t emit_iterations;
+  /* TTFT-SLO-constrained ranking (BASELINE configs[2]; the reference ranks
+     without an SLO, simulator.cpp:277-294, and the paper's SLO use case is
+     PAPER.md:607-615).  ttft_slo > 0: an entry meets the SLO iff it completed
+     requests and the nearest-rank slo_quantile of its per-request TTFT
+     (the p95 rule of simulator.cpp:223-225; slo_quantile 0 => 0.99) is
+     <= ttft_slo.  Entries meeting it rank first, each group in the
+     reference's order.  0 => off (the reference's ranking). */
+  double ttft_slo;
+  double slo_quantile;
 } psg_config;
 
 /* plansim::IterationRecord (simulator.hpp:35-42) without the stage vectors,
@@ -216,6 +225,10 @@ typedef struct psg_entry {
   /* additive outputs the reference does not compute (nearest-rank rule of
      simulator.cpp:223-225 applied at 0.50 / 0.99) */
   double p50_ttft, p99_ttft, p50_tpot, p99_tpot;
+  /* TTFT at config.slo_quantile (nearest rank) and whether the entry meets
+     config.ttft_slo (1), misses it (0); both 0 when the SLO is off */
+  double slo_ttft;
+  int64_t slo_met;
   int64_t per_request_offset;         /* into psg_result.per_request */
   int64_t rejected_offset;            /* into psg_result.rejected_ids */
 } psg_entry;
@@ -226,7 +239,7 @@ typedef struct psg_rank_key {
   double objective_metric;
   double other_metric;
   int32_t enc_rank;
-  int32_t pad_;
+  int32_t slo_miss;                   /* 1: misses config.ttft_slo (ranks after every entry that meets it) */
   double freq_ghz;
   int64_t entry_index;
 } psg_rank_key;
@@ -324,6 +337,9 @@ typedef struct psg_plan_record {
 typedef struct psg_context psg_context;
 
 const char* psg_version(void);
+
+/* Visible CUDA devices (0 and PSG_OK when there are none). */
+int psg_device_count(int* count);
 
 /* One context per device; a context is not thread-shared. */
 int psg_context_create(int device, psg_context** out);

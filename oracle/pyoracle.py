@@ -80,7 +80,8 @@ REF_ENTRY_FIELDS = ("plan_index", "freq_ghz", "e2e_latency", "total_energy", "p9
 
 def read_refdump(path: str):
     """-> (entries: list[dict], warnings: list[str]); each entry carries
-    'encoding', 'per_request' (METRICS_DTYPE array) and 'rejected' (int64)."""
+    'encoding', 'per_request' (METRICS_DTYPE array) and 'rejected' (int64), or
+    for a --digest dump (version 2) their SHA-256 hex digests and lengths."""
     from paper_2411_17651_b200 import abi
     with open(path, "rb") as f:
         data = f.read()
@@ -95,11 +96,20 @@ def read_refdump(path: str):
         (ln,) = struct.unpack_from("<q", data, off); off += 8
         e["encoding"] = data[off:off + ln].decode(); off += ln
         (npr,) = struct.unpack_from("<q", data, off); off += 8
-        e["per_request"] = np.frombuffer(data, dtype=abi.METRICS_DTYPE, count=npr, offset=off).copy()
-        off += 40 * npr
+        if ver == 2:  # --digest: SHA-256 of the arrays' bytes
+            e["n_per_request"] = npr
+            e["per_request_sha256"] = data[off:off + 32].hex(); off += 32
+        else:
+            e["per_request"] = np.frombuffer(data, dtype=abi.METRICS_DTYPE, count=npr,
+                                             offset=off).copy()
+            off += 40 * npr
         (nrj,) = struct.unpack_from("<q", data, off); off += 8
-        e["rejected"] = np.frombuffer(data, dtype="<i8", count=nrj, offset=off).copy()
-        off += 8 * nrj
+        if ver == 2:
+            e["n_rejected"] = nrj
+            e["rejected_sha256"] = data[off:off + 32].hex(); off += 32
+        else:
+            e["rejected"] = np.frombuffer(data, dtype="<i8", count=nrj, offset=off).copy()
+            off += 8 * nrj
         entries.append(e)
     (nw,) = struct.unpack_from("<q", data, off); off += 8
     warns = []

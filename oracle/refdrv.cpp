@@ -11,7 +11,7 @@
 //
 // usage:
 //   refdrv search   <inputs> [sim flags] [--jobs N] [--repeat R] [--plans a:b]
-//                   [--out-result F] [--out-plans F] [--out-store F] [--out-trace F]
+//                   [--no-search] [--out-result F [--digest]] [--out-plans F] [--out-store F] [--out-trace F]
 //   refdrv simulate <inputs> [sim flags] --plan-spec dp,pp,mode:cdp:intra,...
 //                   [--out-result F] [--emit-iterations F]
 //   refdrv sweep    <inputs> [sim flags] --plan-spec ... --segments N [--subset M]
@@ -61,6 +61,8 @@ struct Args {
   std::string anchor = "arrival";
   double reserve = 0.10;
   bool no_embedding = false;
+  bool digest = false;
+  bool no_search = false;
   int max_combos = 65536;
   int jobs = 1, repeat = 1;
   long long plan_lo = 0, plan_hi = -1;
@@ -115,6 +117,8 @@ Args parse(int argc, char** argv) {
       a.plan_hi = std::stoll(s.substr(c + 1));
     } else if (k == "--plan-spec") a.plan_spec = v();
     else if (k == "--out-result") a.out_result = v();
+    else if (k == "--digest") a.digest = true;
+    else if (k == "--no-search") a.no_search = true;
     else if (k == "--out-plans") a.out_plans = v();
     else if (k == "--out-store") a.out_store = v();
     else if (k == "--out-trace") a.out_trace = v();
@@ -167,6 +171,54 @@ Trace load_or_synth_trace(const Args& a) {
 }
 
 // ---- binary result dump (read by tests/refdump.py) -------------------------
+// SHA-256 (FIPS 180-4) of a byte string: the digest form of the result dump
+// (--digest) for traces whose per-request arrays are too large to dump.
+std::string sha256(const std::string& msg) {
+  static const uint32_t K[64] = {
+      0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+      0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+      0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+      0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+      0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+      0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+      0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+      0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+  uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                   0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+  std::string m = msg;
+  const uint64_t bits = uint64_t(msg.size()) * 8;
+  m.push_back(char(0x80));
+  while (m.size() % 64 != 56) m.push_back(char(0));
+  for (int i = 7; i >= 0; --i) m.push_back(char((bits >> (8 * i)) & 0xff));
+  auto rotr = [](uint32_t x, int n) { return (x >> n) | (x << (32 - n)); };
+  for (size_t off = 0; off < m.size(); off += 64) {
+    uint32_t w[64];
+    for (int i = 0; i < 16; ++i)
+      w[i] = uint32_t(uint8_t(m[off + 4 * i])) << 24 | uint32_t(uint8_t(m[off + 4 * i + 1])) << 16 |
+             uint32_t(uint8_t(m[off + 4 * i + 2])) << 8 | uint32_t(uint8_t(m[off + 4 * i + 3]));
+    for (int i = 16; i < 64; ++i) {
+      const uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+      const uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+      w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    for (int i = 0; i < 64; ++i) {
+      const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+      const uint32_t ch = (e & f) ^ (~e & g);
+      const uint32_t t1 = hh + S1 + ch + K[i] + w[i];
+      const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+      const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+      const uint32_t t2 = S0 + mj;
+      hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+  }
+  std::string out;
+  for (uint32_t v : h)
+    for (int i = 3; i >= 0; --i) out.push_back(char((v >> (8 * i)) & 0xff));
+  return out;
+}
+
 struct Writer {
   std::string buf;
   void i64(long long v) { buf.append(reinterpret_cast<const char*>(&v), 8); }
@@ -178,7 +230,7 @@ struct Writer {
 };
 
 void dump_report(Writer& w, long long plan_index, double freq,
-                 const SimulationReport& r) {
+                 const SimulationReport& r, bool digest) {
   w.i64(plan_index);
   w.f64(freq);
   w.f64(r.e2e_latency);
@@ -193,28 +245,33 @@ void dump_report(Writer& w, long long plan_index, double freq,
   w.i64(r.num_iterations);
   w.i64(r.max_batch_observed);
   w.str(r.plan_encoding);
+  Writer pr, rj;
+  Writer& a = digest ? pr : w;
+  Writer& b = digest ? rj : w;
   w.i64((long long)r.per_request.size());
   for (const auto& m : r.per_request) {
-    w.i64(m.id);
-    w.f64(m.ttft);
-    w.f64(m.tpot);
-    w.f64(m.e2e);
-    w.i64(m.gen_len);
+    a.i64(m.id);
+    a.f64(m.ttft);
+    a.f64(m.tpot);
+    a.f64(m.e2e);
+    a.i64(m.gen_len);
   }
+  if (digest) w.buf.append(sha256(pr.buf));
   w.i64((long long)r.rejected_ids.size());
-  for (long long id : r.rejected_ids) w.i64(id);
+  for (long long id : r.rejected_ids) b.i64(id);
+  if (digest) w.buf.append(sha256(rj.buf));
 }
 
 void write_result(const std::string& path,
                   const std::vector<std::pair<long long, double>>& keys,
                   const std::vector<const SimulationReport*>& reports,
-                  const ProfileStore& store) {
+                  const ProfileStore& store, bool digest = false) {
   Writer w;
   w.buf.append("PSGR", 4);
-  w.i64(1);
+  w.i64(digest ? 2 : 1);  // 2: per-request / rejected arrays as SHA-256 digests
   w.i64((long long)reports.size());
   for (size_t i = 0; i < reports.size(); ++i)
-    dump_report(w, keys[i].first, keys[i].second, *reports[i]);
+    dump_report(w, keys[i].first, keys[i].second, *reports[i], digest);
   const auto warns = store.warnings();
   w.i64((long long)warns.size());
   for (const auto& s : warns) w.str(s);
@@ -370,6 +427,10 @@ int run(const Args& a) {
     plans = std::vector<ExecutionPlan>(plans.begin() + lo, plans.begin() + hi);
   }
   if (!a.out_plans.empty()) write_file(a.out_plans, plans_json(plans));
+  if (a.no_search) {  // generate_plans only (input-parity tests)
+    std::printf("{\"cmd\":\"search\",\"plans\":%zu,\"searched\":false}\n", plans.size());
+    return 0;
+  }
   const Objective obj =
       a.objective == "energy" ? Objective::Energy : Objective::Latency;
 
@@ -399,7 +460,7 @@ int run(const Args& a) {
       keys.push_back({(long long)e.plan_index, e.freq_ghz});
       reps.push_back(&e.report);
     }
-    write_result(a.out_result, keys, reps, store);
+    write_result(a.out_result, keys, reps, store, a.digest);
   }
   std::printf(
       "{\"cmd\":\"search\",\"plans\":%zu,\"plans_total\":%zu,\"entries\":%zu,"

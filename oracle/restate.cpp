@@ -16,6 +16,9 @@
 //   BatchState         src/batching.cpp:11-125
 //   query_time/energy  src/cost.cpp:85-102, :196-291
 //   op_flops/op_bytes  src/cost.cpp:51-68
+//   TTFT-SLO ranking   an addition (psg.h psg_config.ttft_slo); unpinned by the
+//                      reference, which has no SLO; tests derive it from the
+//                      reference's own per-request TTFTs instead
 // Deliberately naive: std::deque / std::vector state, per-query key lookup,
 // O(B) ledger recomputation — no event skipping, so it is an independent
 // check of the GPU engine's macro-stepping.
@@ -393,6 +396,12 @@ EntryResult simulate(const Plan& pl, const psg_cluster* cl, const psg_trace* T,
       e.p50_tpot = nearest(tpot, 0.50);
       e.p99_tpot = nearest(tpot, 0.99);
     }
+    // TTFT-SLO-constrained ranking (psg.h psg_config.ttft_slo): nearest-rank
+    // quantile of TTFT, the p95 rule of simulator.cpp:223-225
+    if (cfg->ttft_slo > 0.0) {
+      e.slo_ttft = nearest(ttft, cfg->slo_quantile > 0.0 ? cfg->slo_quantile : 0.99);
+      e.slo_met = e.slo_ttft <= cfg->ttft_slo ? 1 : 0;
+    }
   }
   if (e.e2e_latency > 0) {
     const int dt = P->compute_dtype[pl.p];
@@ -456,6 +465,7 @@ int oracle_search(const psg_plan_set* P, const psg_cluster* cl, const psg_store*
     std::sort(order.begin(), order.end(), [&](size_t ia, size_t ib) {
       const psg_entry& a = res[ia].e;
       const psg_entry& b = res[ib].e;
+      if (a.slo_met != b.slo_met) return a.slo_met > b.slo_met;  // SLO met first (0 when off)
       if (a.num_rejected != b.num_rejected) return a.num_rejected < b.num_rejected;
       if (obj(a, lat) != obj(b, lat)) return obj(a, lat) < obj(b, lat);
       if (obj(a, !lat) != obj(b, !lat)) return obj(a, !lat) < obj(b, !lat);

@@ -8,7 +8,7 @@
 // usage: shim_parity --model F --cluster F (--profiles F | --synth-profiles X)
 //        (--trace F | --synth-trace a,b,c,d,rate,n,seed) [--objective energy]
 //        [--freqs a,b] [--batching chunked --chunk N] [--max-batch N]
-//        [--anchor admission] [--jobs N] [--drop-table OP]
+//        [--anchor admission] [--jobs N] [--threads T] [--drop-table OP]
 //        [--single K [--sweep-segments S --sweep-subset M]]
 // --single K additionally compares simulate_plan(plans[K]) with
 // emit_iterations (every IterationRecord) and, with --sweep-segments,
@@ -21,6 +21,7 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "plansim/simulator.hpp"
@@ -47,6 +48,45 @@ std::string drop_lines(const std::string& text, const std::string& needle) {
   return out.str();
 }
 
+// Mismatches between two rankings (every report field, per-request metrics, rejected ids).
+int diff_ranked(const RankedPlans& a, const RankedPlans& b, std::string& first) {
+  int bad = 0;
+  auto miss = [&](const std::string& what) {
+    if (!bad++) first = what;
+  };
+  if (a.entries.size() != b.entries.size()) miss("entry count");
+  for (size_t i = 0; i < a.entries.size() && i < b.entries.size(); ++i) {
+    const auto& x = a.entries[i];
+    const auto& y = b.entries[i];
+    const auto& r = x.report;
+    const auto& g = y.report;
+    const std::string at = " at rank " + std::to_string(i) + " " + r.plan_encoding;
+    if (x.plan_index != y.plan_index || x.freq_ghz != y.freq_ghz) miss("entry identity" + at);
+    if (r.plan_encoding != g.plan_encoding || r.frequency_ghz != g.frequency_ghz) miss("encoding" + at);
+    if (r.e2e_latency != g.e2e_latency || r.total_energy != g.total_energy ||
+        r.p95_latency != g.p95_latency || r.mean_ttft != g.mean_ttft || r.mean_tpot != g.mean_tpot)
+      miss("latency/energy/ttft/tpot" + at);
+    if (r.mfu != g.mfu || r.mbu != g.mbu) miss("mfu/mbu" + at);
+    if (r.num_completed != g.num_completed || r.num_rejected != g.num_rejected ||
+        r.num_iterations != g.num_iterations || r.max_batch_observed != g.max_batch_observed)
+      miss("counters" + at);
+    if (r.rejected_ids != g.rejected_ids) miss("rejected ids" + at);
+    if (r.per_request.size() != g.per_request.size()) {
+      miss("per_request size" + at);
+    } else {
+      for (size_t k = 0; k < r.per_request.size(); ++k) {
+        const auto& p = r.per_request[k];
+        const auto& q = g.per_request[k];
+        if (p.id != q.id || p.ttft != q.ttft || p.tpot != q.tpot || p.e2e != q.e2e || p.gen_len != q.gen_len) {
+          miss("per_request" + at);
+          break;
+        }
+      }
+    }
+  }
+  return bad;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -54,7 +94,7 @@ int main(int argc, char** argv) {
   double synth_ctx = 0;
   std::vector<double> synth_tr, freqs;
   SimConfig cfg;
-  int jobs = 1, single = -1, sweep_segments = 0;
+  int jobs = 1, single = -1, sweep_segments = 0, threads = 1;
   long long sweep_subset = 256;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -71,6 +111,7 @@ int main(int argc, char** argv) {
     else if (k == "--max-batch") cfg.policy.max_batch_size = std::stoll(v);
     else if (k == "--anchor") cfg.ttft_anchor = v == "admission" ? TtftAnchor::Admission : TtftAnchor::Arrival;
     else if (k == "--jobs") jobs = std::stoi(v);
+    else if (k == "--threads") threads = std::stoi(v);
     else if (k == "--drop-table") drop = v;
     else if (k == "--single") single = std::stoi(v);
     else if (k == "--sweep-segments") sweep_segments = std::stoi(v);
@@ -121,34 +162,34 @@ int main(int argc, char** argv) {
     auto miss = [&](const std::string& what) {
       if (!bad++) first = what;
     };
-    if (a.entries.size() != b.entries.size()) miss("entry count");
-    for (size_t i = 0; i < a.entries.size() && i < b.entries.size(); ++i) {
-      const auto& x = a.entries[i];
-      const auto& y = b.entries[i];
-      const auto& r = x.report;
-      const auto& g = y.report;
-      const std::string at = " at rank " + std::to_string(i) + " " + r.plan_encoding;
-      if (x.plan_index != y.plan_index || x.freq_ghz != y.freq_ghz) miss("entry identity" + at);
-      if (r.plan_encoding != g.plan_encoding || r.frequency_ghz != g.frequency_ghz) miss("encoding" + at);
-      if (r.e2e_latency != g.e2e_latency || r.total_energy != g.total_energy ||
-          r.p95_latency != g.p95_latency || r.mean_ttft != g.mean_ttft || r.mean_tpot != g.mean_tpot)
-        miss("latency/energy/ttft/tpot" + at);
-      if (r.mfu != g.mfu || r.mbu != g.mbu) miss("mfu/mbu" + at);
-      if (r.num_completed != g.num_completed || r.num_rejected != g.num_rejected ||
-          r.num_iterations != g.num_iterations || r.max_batch_observed != g.max_batch_observed)
-        miss("counters" + at);
-      if (r.rejected_ids != g.rejected_ids) miss("rejected ids" + at);
-      if (r.per_request.size() != g.per_request.size()) {
-        miss("per_request size" + at);
-      } else {
-        for (size_t k = 0; k < r.per_request.size(); ++k) {
-          const auto& p = r.per_request[k];
-          const auto& q = g.per_request[k];
-          if (p.id != q.id || p.ttft != q.ttft || p.tpot != q.tpot || p.e2e != q.e2e || p.gen_len != q.gen_len) {
-            miss("per_request" + at);
-            break;
+    {
+      std::string f;
+      if (const int d = diff_ranked(a, b, f)) {
+        bad += d - 1;
+        miss(f);
+      }
+    }
+    // concurrent callers of the drop-in (each with its own store: clamp
+    // replays write its warnings) get the single caller's result
+    if (threads > 1) {
+      std::vector<RankedPlans> got(static_cast<size_t>(threads));
+      std::vector<std::string> errs(static_cast<size_t>(threads));
+      std::vector<std::thread> th;
+      for (int t = 0; t < threads; ++t)
+        th.emplace_back([&, t] {
+          try {
+            std::istringstream st(store_text);
+            const ProfileStore own = ProfileStore::load(st);
+            got[size_t(t)] = plansim_gpu::search(plans, model, cluster, trace, own, obj, freqs, cfg, jobs);
+          } catch (const std::exception& e) {
+            errs[size_t(t)] = e.what();
           }
-        }
+        });
+      for (auto& x : th) x.join();
+      for (int t = 0; t < threads; ++t) {
+        std::string f;
+        if (!errs[size_t(t)].empty()) miss("thread " + std::to_string(t) + ": " + errs[size_t(t)]);
+        else if (diff_ranked(b, got[size_t(t)], f)) miss("thread " + std::to_string(t) + ": " + f);
       }
     }
     size_t n_iter = 0, n_rows = 0;

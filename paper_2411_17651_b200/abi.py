@@ -66,7 +66,8 @@ class ConfigC(C.Structure):
                 ("ttft_anchor", C.c_int32), ("n_freqs", C.c_int32),
                 ("freqs", _f64p), ("detail", C.c_int32), ("rank", C.c_int32),
                 ("n_entry_subset", C.c_int32), ("entry_subset", _i32p),
-                ("entry_max_batch_size", _i64p), ("emit_iterations", C.c_int32)]
+                ("entry_max_batch_size", _i64p), ("emit_iterations", C.c_int32),
+                ("ttft_slo", C.c_double), ("slo_quantile", C.c_double)]
 
 
 ENTRY_DTYPE = np.dtype([
@@ -75,15 +76,21 @@ ENTRY_DTYPE = np.dtype([
     ("mean_ttft", "<f8"), ("mean_tpot", "<f8"), ("mfu", "<f8"), ("mbu", "<f8"),
     ("num_completed", "<i8"), ("num_rejected", "<i8"), ("num_iterations", "<i8"),
     ("max_batch_observed", "<i8"), ("p50_ttft", "<f8"), ("p99_ttft", "<f8"),
-    ("p50_tpot", "<f8"), ("p99_tpot", "<f8"), ("per_request_offset", "<i8"),
+    ("p50_tpot", "<f8"), ("p99_tpot", "<f8"), ("slo_ttft", "<f8"), ("slo_met", "<i8"),
+    ("per_request_offset", "<i8"),
     ("rejected_offset", "<i8")])
 METRICS_DTYPE = np.dtype([("id", "<i8"), ("ttft", "<f8"), ("tpot", "<f8"),
                           ("e2e", "<f8"), ("gen_len", "<i8")])
 ITERATION_DTYPE = np.dtype([("clock_start", "<f8"), ("duration", "<f8"), ("energy", "<f8"),
                             ("batch_size", "<i8")])
 RANK_KEY_DTYPE = np.dtype([("num_rejected", "<i8"), ("objective_metric", "<f8"),
-                           ("other_metric", "<f8"), ("enc_rank", "<i4"), ("pad_", "<i4"),
+                           ("other_metric", "<f8"), ("enc_rank", "<i4"), ("slo_miss", "<i4"),
                            ("freq_ghz", "<f8"), ("entry_index", "<i8")])
+
+
+def empty_rank_keys():
+    """A zero-length psg_rank_key array (an empty shard's contribution)."""
+    return np.zeros(0, dtype=RANK_KEY_DTYPE)
 
 
 class ResultC(C.Structure):

@@ -168,6 +168,8 @@ RankedPlans run(const std::vector<ExecutionPlan>& plans, const ClusterSpec& clus
   c.entry_subset = o.subset.empty() ? nullptr : o.subset.data();
   c.entry_max_batch_size = o.caps.empty() ? nullptr : o.caps.data();
   c.emit_iterations = o.emit ? 1 : 0;
+  c.ttft_slo = cfg.ttft_slo;
+  c.slo_quantile = cfg.slo_quantile;
   psg_result* res = nullptr;
   const int rc = psg_search(engine->handle(), &soa.view(), &cl, &store.view(), &tr.view, &c, &res);
   if (rc != PSG_OK) raise(rc, psg_last_error(engine->handle()));
@@ -197,6 +199,8 @@ RankedPlans run(const std::vector<ExecutionPlan>& plans, const ClusterSpec& clus
     r.p99_ttft = e.p99_ttft;
     r.p50_tpot = e.p50_tpot;
     r.p99_tpot = e.p99_tpot;
+    r.slo_ttft = e.slo_ttft;
+    r.slo_met = e.slo_met != 0;
     r.per_request.resize(size_t(e.num_completed));
     if (e.num_completed)
       std::memcpy(r.per_request.data(), res->per_request + e.per_request_offset,

@@ -17,7 +17,7 @@ namespace psg {
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxCells = 8;      // cells per block (the reference IR emits 2)
-constexpr int kMaxClampSlots = 64;  // cells + collectives + p2p boundaries
+constexpr int kMaxClampSlots = 64;  // collectives + distinct p2p curves of a plan
 constexpr int kWindow = 32;         // prefetched upcoming requests per unit
 constexpr int kProfSlots = 26;      // phase-profile counters per unit (dev builds)
 
@@ -62,6 +62,8 @@ struct Unit {
   int32_t n_req;       // requests in this replica
   int64_t seq_base;    // offset into DTrace::seq (if used)
   int64_t scratch;     // offset (elements) into the per-unit global scratch
+  int64_t gtab;        // staged curves in SimParams::g_tab at this offset (doubles), or -1:
+                       // shared memory (they fit the launch's per-unit budget)
 };
 
 struct UnitOut {
@@ -80,6 +82,8 @@ struct SimParams {
   const int32_t* cell_tab;   // [n_freq_slots * n_cells_total]
   const int32_t* coll_tab;   // [n_colls_total]
   const int32_t* p2p_tab;    // [n_p2p_total]
+  const uint8_t* p2p_bslot;  // [n_p2p_total] boundary -> distinct p2p curve of its plan
+  double* g_tab;             // global curve staging of units whose curves exceed tab_smem
   const int32_t* entry_missing;  // per local entry: 1 if any table it queries is absent
   int32_t n_cells_total;
   const Unit* units;

@@ -152,7 +152,7 @@ struct psg_context {
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
-  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan;
+  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan, d_gtab;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
   std::vector<uint8_t> compute_clamp, curve_clamp;
@@ -334,6 +334,14 @@ extern "C" {
 
 const char* psg_version(void) { return "psg-b200 1 (sm_100a)"; }
 
+int psg_device_count(int* count) {
+  if (!count) return PSG_ERR_USAGE;
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  *count = c;
+  return PSG_OK;
+}
+
 int psg_context_create(int device, psg_context** out) {
   if (!out) return PSG_ERR_USAGE;
   *out = nullptr;
@@ -379,7 +387,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
                     &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
-                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan})
+                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan, &ctx->d_gtab})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj, &ctx->h_it, &ctx->h_isec, &ctx->h_ijou})
     b->release();
@@ -453,6 +461,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   const int E = int(ent.size());
   if (cfg->emit_iterations && E != 1)
     return fail(ctx, PSG_ERR_USAGE, "emit_iterations requires exactly one (plan, frequency) entry");
+  if (!(cfg->ttft_slo >= 0.0) || !(cfg->slo_quantile >= 0.0 && cfg->slo_quantile <= 1.0))
+    return fail(ctx, PSG_ERR_USAGE, "ttft_slo must be >= 0 and slo_quantile in [0, 1]");
 
   // ---- validate plans ----
   const int np = P->n_plans;
@@ -461,7 +471,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     const int C = P->cell_begin[p + 1] - P->cell_begin[p];
     const int K = P->coll_begin[p + 1] - P->coll_begin[p];
     const int NB = P->p2p_begin[p + 1] - P->p2p_begin[p];
-    if (C < 0 || K < 0 || NB < 0 || C > kMaxCells || C + K + NB > kMaxClampSlots)
+    if (C < 0 || K < 0 || NB < 0 || C > kMaxCells || K > kMaxClampSlots)
       return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": unsupported cell/collective count");
     if (P->model_dp[p] < 1 || P->num_stages[p] < 1)
       return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": bad degrees");
@@ -497,6 +507,30 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   for (int b = 0; b < n_p2p; ++b) {
     auto it = kmap.find({int(PSG_COLL_P2P), 2, P->p2p_nodes[b]});
     p2p_tab[b] = it == kmap.end() ? -1 : it->second;
+  }
+  // Stage boundaries share a handful of distinct p2p curves (one per node
+  // span, planner.cpp:344): boundary -> distinct curve in first-appearance
+  // order (the simulation kernel's rule), and per plan the doubles its staged
+  // curves take (knots + seconds/joules of the collectives and distinct p2p).
+  std::vector<uint8_t> bslot(std::max(n_p2p, 1), 0);
+  std::vector<int64_t> plan_tab_need(np, 0);
+  for (int p = 0; p < np; ++p) {
+    std::vector<int32_t> distinct;
+    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b) {
+      size_t s = 0;
+      while (s < distinct.size() && distinct[s] != p2p_tab[b]) ++s;
+      if (s == distinct.size()) distinct.push_back(p2p_tab[b]);
+      bslot[b] = uint8_t(std::min<size_t>(s, 255));
+    }
+    const int K = P->coll_begin[p + 1] - P->coll_begin[p];
+    if (K + int(distinct.size()) > kMaxClampSlots)
+      return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": more than " +
+                                          std::to_string(kMaxClampSlots) + " distinct curves");
+    int64_t need = 0;
+    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1]; ++k)
+      need += 3 * int64_t(coll_tab[k] >= 0 ? S->k_n[coll_tab[k]] : 1);
+    for (int32_t t : distinct) need += 3 * int64_t(t >= 0 ? S->k_n[t] : 1);
+    plan_tab_need[p] = need;
   }
   std::vector<int32_t> entry_missing(E, 0);
   std::vector<std::string> missing_msg(E);
@@ -538,6 +572,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     if (T->context_len[i] < 0 || T->context_len[i] >= (int64_t(1) << 26) ||
         T->gen_len[i] >= (int64_t(1) << 26))
       return fail(ctx, PSG_ERR_USAGE, "trace lengths outside the supported range [0, 2^26)");
+    // a non-finite arrival has no place in the clock order (the decode-run
+    // horizon compares it against finite clocks)
+    if (!std::isfinite(T->arrival[i]))
+      return fail(ctx, PSG_ERR_USAGE, "trace arrivals must be finite");
     tok_total += T->context_len[i] + std::max<int64_t>(T->gen_len[i], 1);
     if (i && T->arrival[i] < T->arrival[i - 1]) sorted = false;
   }
@@ -598,6 +636,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       u.seq_base = sorted ? 0 : seq_base_of[R] + off;
       off += u.n_req;
       u.scratch = 0;
+      u.gtab = -1;
       units.push_back(u);
     }
   }
@@ -702,22 +741,18 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     ent_plan[e] = int32_t(ent[e] / F);
     ent_fslot[e] = int32_t(ent[e] % F);
   }
-  if (max_qrows > int64_t(65535) * 256 || max_drows > int64_t(65535) * 256)
-    return fail(ctx, PSG_ERR_USAGE, "trace too long for the cost-table grid");
-  // curves staged per unit in shared memory
-  size_t tab_cap = 1;
-  for (int e = 0; e < E; ++e) {
-    const int p = int(ent[e] / F);
-    size_t need = 0;
-    for (int k = P->coll_begin[p]; k < P->coll_begin[p + 1]; ++k)
-      need += 3 * size_t(coll_tab[k] >= 0 ? S->k_n[coll_tab[k]] : 1);
-    for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b)
-      need += 3 * size_t(p2p_tab[b] >= 0 ? S->k_n[p2p_tab[b]] : 1);
-    tab_cap = std::max(tab_cap, need);
+  // curves staged per unit in shared memory up to 96 KB; a plan with larger
+  // curves stages them in the unit's global region instead
+  constexpr int64_t kTabSmemCap = 96 * 1024 / int64_t(sizeof(double));
+  int64_t tab_cap = 1;
+  for (int e = 0; e < E; ++e) tab_cap = std::max(tab_cap, plan_tab_need[ent[e] / F]);
+  const int tab_smem = int(std::min(tab_cap, kTabSmemCap));
+  int64_t gtab_total = 0;
+  for (auto& u : units) {
+    const int64_t need = plan_tab_need[u.plan];
+    u.gtab = need > tab_smem ? gtab_total : -1;
+    if (need > tab_smem) gtab_total += (need + 1) & ~int64_t(1);
   }
-  if (tab_cap * sizeof(double) > 96 * 1024)
-    return fail(ctx, PSG_ERR_USAGE, "collective curves of one plan exceed on-chip staging (96 KB)");
-  const int tab_smem = int(tab_cap);
 
   // ---- pack inputs ----
   Packer pk;
@@ -755,6 +790,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                o_celltab = pk.add(cell_tab.data(), cell_tab.size()),
                o_colltab = pk.add(coll_tab.data(), coll_tab.size()),
                o_p2ptab = pk.add(p2p_tab.data(), p2p_tab.size()),
+               o_bslot = pk.add(bslot.data(), bslot.size()),
                o_emiss = pk.add(entry_missing.data(), E),
                o_units = pk.add(units.data(), units.size()),
                o_eub = pk.add(entry_unit_begin.data(), E + 1),
@@ -829,6 +865,9 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.cell_tab = (const int32_t*)D(o_celltab);
   sp.coll_tab = (const int32_t*)D(o_colltab);
   sp.p2p_tab = (const int32_t*)D(o_p2ptab);
+  sp.p2p_bslot = (const uint8_t*)D(o_bslot);
+  PSG_CUDA(ctx->d_gtab.ensure(size_t(std::max<int64_t>(gtab_total, 1)) * sizeof(double)));
+  sp.g_tab = static_cast<double*>(ctx->d_gtab.p);
   sp.entry_missing = (const int32_t*)D(o_emiss);
   sp.n_cells_total = n_cells;
   sp.units = (const Unit*)D(o_units);
@@ -956,6 +995,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   rp.total_devices = cl->total_devices;
   rp.objective = cfg->objective;
   rp.extras = 1;
+  rp.ttft_slo = cfg->ttft_slo > 0.0 ? cfg->ttft_slo : 0.0;
+  rp.slo_quantile = cfg->slo_quantile > 0.0 ? cfg->slo_quantile : 0.99;
   rp.chain_replicas = sp.chain_replicas;
   sp.entry_unit_begin = rp.entry_unit_begin;
   sp.entry_units = rp.entry_units;
@@ -976,11 +1017,14 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   const size_t smem = sim_smem_bytes(sp.smem_cap, sp.memo_cap, sp.tab_smem, sp.cm2_cap);
   if (prof_path) std::fprintf(stderr, "psg: units=%d smem_cap=%d smem=%zu B\n", n_units, sp.smem_cap, smem);
   if (n_sig > 0) {  // cell-query tables, then decode-only iteration tables
-    qtab_kernel<<<dim3(unsigned(n_sig), unsigned((max_qrows + 255) / 256)), 256, 0, st>>>(tp);
+    // grid.y covers the longest table (row loops in the kernels beyond 65535 x 256)
+    qtab_kernel<<<dim3(unsigned(n_sig), unsigned(std::min<int64_t>((max_qrows + 255) / 256, 65535))),
+                  256, 0, st>>>(tp);
     ++launches;
   }
   if (E > 0) {
-    dectab_kernel<<<dim3(unsigned(E), unsigned((max_drows + 255) / 256)), 256, 0, st>>>(tp);
+    dectab_kernel<<<dim3(unsigned(E), unsigned(std::min<int64_t>((max_drows + 255) / 256, 65535))),
+                    256, 0, st>>>(tp);
     ++launches;
   }
   if (n_units > 0) {
@@ -1142,6 +1186,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     r.p99_ttft = o.p99_ttft;
     r.p50_tpot = o.p50_tpot;
     r.p99_tpot = o.p99_tpot;
+    r.slo_ttft = o.slo_ttft;
+    r.slo_met = rp.ttft_slo > 0.0 && o.completed > 0 && o.slo_ttft <= rp.ttft_slo ? 1 : 0;
     r.per_request_offset = cfg->detail ? proff[e] : 0;
     r.rejected_offset = cfg->detail ? rjoff[e] : 0;
   }

@@ -9,7 +9,8 @@
 //  compact_kernel       per_request sorted by id / rejected_ids sorted
 //                       (simulator.cpp:205-207) as dense arrays for one D2H.
 //  rank_kernel          search()'s comparator (simulator.cpp:283-294):
-//                       (num_rejected, objective, other, encoding, freq).
+//                       (num_rejected, objective, other, encoding, freq),
+//                       after the TTFT-SLO flag when an SLO is set.
 #include <cub/block/block_scan.cuh>
 
 #include "psg_device.cuh"
@@ -39,9 +40,10 @@ __device__ __forceinline__ int64_t nearest_rank(double q, int64_t n) {
 
 __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const ReduceParams r) {
   const int e = blockIdx.x;
-  __shared__ unsigned sel_hist[5][256];
-  __shared__ uint64_t sel_prefix[5];
-  __shared__ int64_t sel_k[5];
+  constexpr int kStats = 6;  // p95 e2e, p50/p99 TTFT, p50/p99 TPOT, TTFT at the SLO quantile
+  __shared__ unsigned sel_hist[kStats][256];
+  __shared__ uint64_t sel_prefix[kStats];
+  __shared__ int64_t sel_k[kStats];
   __shared__ double sh_sums[2];
   __shared__ int64_t sh_cnt[2];
 
@@ -155,38 +157,38 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
     }
   }
 
-  // ---- order statistics: p95 latency (simulator.cpp:222-225) and the
-  // p50/p99 TTFT/TPOT extras, all five by one fused MSB radix select: each
-  // 8-bit pass sweeps the slots once and builds the five histograms, one
-  // warp per statistic picks its digit ----
-  double p95 = 0.0, t50 = 0.0, t99 = 0.0, q50 = 0.0, q99 = 0.0;
+  // ---- order statistics: p95 latency (simulator.cpp:222-225), the
+  // p50/p99 TTFT/TPOT extras and the SLO quantile of TTFT, all by one fused
+  // MSB radix select: each 8-bit pass sweeps the slots once and builds the
+  // active statistics' histograms, one warp per statistic picks its digit ----
+  const bool slo = r.ttft_slo > 0.0;
+  double p95 = 0.0, t50 = 0.0, t99 = 0.0, q50 = 0.0, q99 = 0.0, tslo = 0.0;
   if (ncomp > 0) {
-    const int m = r.extras ? (ntpot > 0 ? 5 : 3) : 1;
-    if (threadIdx.x < 5) {
+    const bool ext = r.extras != 0, tp = ext && ntpot > 0;
+    const bool act[kStats] = {true, ext, ext, tp, tp, slo};
+    if (threadIdx.x < kStats) {
       const int j = threadIdx.x;
-      sel_k[j] = j == 0 ? nearest_rank(0.95, ncomp)
-               : j == 1 ? nearest_rank(0.50, ncomp)
-               : j == 2 ? nearest_rank(0.99, ncomp)
-               : j == 3 ? nearest_rank(0.50, ntpot > 0 ? ntpot : 1)
-                        : nearest_rank(0.99, ntpot > 0 ? ntpot : 1);
+      const double q = j == 0 ? 0.95 : (j == 1 || j == 3) ? 0.50 : j == 5 ? r.slo_quantile : 0.99;
+      sel_k[j] = nearest_rank(q, j == 3 || j == 4 ? (ntpot > 0 ? ntpot : 1) : ncomp);
       sel_prefix[j] = 0;
     }
     uint64_t mask = 0;
     for (int pass = 7; pass >= 0; --pass) {
       const int shift = pass * 8;
-      for (int i = threadIdx.x; i < 5 * 256; i += blockDim.x) sel_hist[i / 256][i % 256] = 0;
+      for (int i = threadIdx.x; i < kStats * 256; i += blockDim.x) sel_hist[i / 256][i % 256] = 0;
       __syncthreads();
       const uint64_t pe = sel_prefix[0], pt50 = sel_prefix[1], pt99 = sel_prefix[2],
-                     pp50 = sel_prefix[3], pp99 = sel_prefix[4];
+                     pp50 = sel_prefix[3], pp99 = sel_prefix[4], pslo = sel_prefix[5];
       for (int64_t i = threadIdx.x; i < r.n_slots; i += blockDim.x) {
         if (st[i] != 1) continue;
         const uint64_t ke = order_key(e2e[i]) , m8 = (ke >> shift) & 255u;
         if ((ke & mask) == pe) atomicAdd(&sel_hist[0][m8], 1u);
-        if (m > 1) {
+        if (ext || slo) {
           const uint64_t kt = order_key(ttft[i]), d = (kt >> shift) & 255u;
-          if ((kt & mask) == pt50) atomicAdd(&sel_hist[1][d], 1u);
-          if ((kt & mask) == pt99) atomicAdd(&sel_hist[2][d], 1u);
-          if (m > 3 && gen[i] >= 2) {
+          if (ext && (kt & mask) == pt50) atomicAdd(&sel_hist[1][d], 1u);
+          if (ext && (kt & mask) == pt99) atomicAdd(&sel_hist[2][d], 1u);
+          if (slo && (kt & mask) == pslo) atomicAdd(&sel_hist[5][d], 1u);
+          if (tp && gen[i] >= 2) {
             const uint64_t kp = order_key(tpot[i]), dp = (kp >> shift) & 255u;
             if ((kp & mask) == pp50) atomicAdd(&sel_hist[3][dp], 1u);
             if ((kp & mask) == pp99) atomicAdd(&sel_hist[4][dp], 1u);
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
       }
       __syncthreads();
       const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-      if (w < m) {  // first digit whose inclusive count exceeds k (as the serial scan)
+      if (w < kStats && act[w]) {  // first digit whose inclusive count exceeds k (as the serial scan)
         const int64_t k = sel_k[w];
         unsigned part = 0;
         for (int b = 0; b < 8; ++b) part += sel_hist[w][lane * 8 + b];
@@ -227,14 +229,15 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
       __syncthreads();
     }
     p95 = from_order_key(sel_prefix[0]);
-    if (m > 1) {
+    if (act[1]) {
       t50 = from_order_key(sel_prefix[1]);
       t99 = from_order_key(sel_prefix[2]);
     }
-    if (m > 3) {
+    if (act[3]) {
       q50 = from_order_key(sel_prefix[3]);
       q99 = from_order_key(sel_prefix[4]);
     }
+    if (act[5]) tslo = from_order_key(sel_prefix[5]);
   }
   if (threadIdx.x == 0) {
     o.p95 = p95;
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
     o.p99_ttft = t99;
     o.p50_tpot = q50;
     o.p99_tpot = q99;
+    o.slo_ttft = tslo;
     r.eout[e] = o;
     psg_rank_key k;
     const bool lat = r.objective == PSG_OBJ_LATENCY;
@@ -249,7 +253,8 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
     k.objective_metric = lat ? o.e2e : o.energy;
     k.other_metric = lat ? o.energy : o.e2e;
     k.enc_rank = r.entry_enc_rank[e];
-    k.pad_ = 0;
+    // an entry with no completed request cannot meet a TTFT SLO
+    k.slo_miss = slo && !(ncomp > 0 && tslo <= r.ttft_slo) ? 1 : 0;
     k.freq_ghz = r.entry_freq[e];
     k.entry_index = r.entry_global[e];
     r.keys[e] = k;
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(256) compact_kernel(const ReduceParams r,
 }
 
 __device__ __forceinline__ bool key_less(const psg_rank_key& a, const psg_rank_key& b) {
+  if (a.slo_miss != b.slo_miss) return a.slo_miss < b.slo_miss;  // SLO met first (0 when off)
   if (a.num_rejected != b.num_rejected) return a.num_rejected < b.num_rejected;
   if (a.objective_metric != b.objective_metric) return a.objective_metric < b.objective_metric;
   if (a.other_metric != b.other_metric) return a.other_metric < b.other_metric;

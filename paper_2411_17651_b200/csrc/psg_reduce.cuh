@@ -11,7 +11,7 @@ namespace psg {
 
 struct EntryOut {
   double e2e, energy, flops, bytes, mean_ttft, mean_tpot, mfu, mbu, p95;
-  double p50_ttft, p99_ttft, p50_tpot, p99_tpot;
+  double p50_ttft, p99_ttft, p50_tpot, p99_tpot, slo_ttft;
   int64_t iterations, max_batch, completed, rejected, sum_batch, admissions;
   int32_t err, pad;
 };
@@ -35,6 +35,8 @@ struct ReduceParams {
   int32_t objective;
   int32_t extras;
   int32_t chain_replicas;  // uout flops/bytes are running tallies: take the last replica's
+  double ttft_slo;         // > 0: TTFT-SLO-constrained ranking (psg_config.ttft_slo)
+  double slo_quantile;
   EntryOut* eout;
   psg_rank_key* keys;
 };

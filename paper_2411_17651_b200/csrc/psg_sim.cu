@@ -90,6 +90,8 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 //   PSG_PIPE_MIN  shortest decode run stepped by the software-pipelined loop
 //   PSG_FILL_B    live slots at or below which a finish returns the batch to
 //                 lane-resident slots
+//   PSG_DIRECT_CHUNKS  slot-array finishes of at most this many 32-slot chunks
+//                 finish every chunk at once instead of walking the summary
 #ifndef PSG_REG_ALL
 #define PSG_REG_ALL 0
 #endif
@@ -99,6 +101,9 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 #ifndef PSG_FILL_B
 #define PSG_FILL_B 32
 #endif
+#ifndef PSG_DIRECT_CHUNKS  // slot-array finishes: batches of <= 32x this many slots skip the summary walk
+#define PSG_DIRECT_CHUNKS 4
+#endif
 constexpr int kMemoCap = 256;  // decode-cost memo entries (SimParams::memo_cap must match)
 
 // Fixed-size per-unit state lives in static shared memory: constant addresses,
@@ -106,7 +111,6 @@ constexpr int kMemoCap = 256;  // decode-cost memo entries (SimParams::memo_cap 
 __shared__ __align__(16) double s_qv[4 * kQvStride];              // query values (4 chains)
 __shared__ __align__(16) CurveDesc s_cdesc[kMaxClampSlots];       // staged curves
 __shared__ __align__(16) int64_t s_cellq[kMaxCells];              // qtab row 0 per cell
-__shared__ __align__(16) uint8_t s_p2p_slot[kMaxClampSlots];      // boundary -> distinct p2p curve
 __shared__ __align__(16) double s_p2p_val[2 * kMaxClampSlots];    // p2p (seconds, joules)
 __shared__ __align__(16) double s_w_arr[kWindow];                 // prefetch window: arrival
 __shared__ __align__(16) int32_t s_w_i32[4 * kWindow];            // tidx, ctx, gen, slot
@@ -116,7 +120,7 @@ __shared__ __align__(16) double s_memo[4 * kMemoCap];             // decode-only
 __shared__ __align__(16) unsigned long long s_rkey[4 * kMemoCap];
 
 struct SmemLayout {
-  size_t qv, cdesc, cellq, p2p_slot, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
+  size_t qv, cdesc, cellq, p2p_val, win_arr, win_i32, memo, act_f64, act_fin, act_i32,
       cm1, cm2, tab, total;
 };
 
@@ -124,7 +128,7 @@ __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_s
   SmemLayout L;
   size_t o = 0;
   (void)memo_cap;  // the fixed-size state is static shared memory (above)
-  L.qv = L.cdesc = L.cellq = L.p2p_slot = L.p2p_val = L.win_arr = L.win_i32 = L.memo = 0;
+  L.qv = L.cdesc = L.cellq = L.p2p_val = L.win_arr = L.win_i32 = L.memo = 0;
   L.act_f64 = o;   o = al16(o + sizeof(double) * 3 * size_t(smem_cap));
   L.act_fin = o;   o = al16(o + sizeof(int64_t) * size_t(smem_cap));
   L.act_i32 = o;   o = al16(o + sizeof(int32_t) * 6 * size_t(smem_cap));
@@ -139,7 +143,9 @@ __host__ __device__ SmemLayout smem_layout(int smem_cap, int memo_cap, int tab_s
 // copy in shared memory for the speculation warp).
 struct EvalCtx {
   const double* qtab;
-  uint64_t p2p_mask;
+  const double* tab;      // the unit's staged curves (shared memory, or global if too large)
+  const uint8_t* bslot;   // boundary -> distinct p2p curve (global, first-appearance order)
+  uint64_t p2p_mask;      // the same for boundaries 0..63 when ND <= 2
   double sdd, reps, Sd;
   int C, K, NQ, ND, NB, n_curve_knots;
 };
@@ -258,7 +264,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
   o.jrep = __dmul_rn(bj, E.reps);
   double cd = dmax_ref(0.0, o.srep);
   double ce = __dadd_rn(0.0, o.jrep);
-  if (E.ND <= 2) {
+  if (E.ND <= 2 && E.NB <= 64) {
     const double s0 = __dadd_rn(o.srep, p2p_val[0]), s1 = __dadd_rn(o.srep, p2p_val[1]);
     const double j0 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots]);
     const double j1 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + 1]);
@@ -267,7 +273,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
     for (int b = 0; b < E.NB; ++b) ce = __dadd_rn(ce, ((E.p2p_mask >> b) & 1) ? j1 : j0);
   } else {
     for (int b = 0; b < E.NB; ++b) {
-      const int s = p2p_slot[b];
+      const int s = __ldg(p2p_slot + b);
       cd = dmax_ref(cd, __dadd_rn(o.srep, p2p_val[s]));
       ce = __dadd_rn(ce, __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + s]));
     }
@@ -372,12 +378,14 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   double* qv = s_qv;
   CurveDesc* cdesc = s_cdesc;
   int64_t* cellq = s_cellq;
-  uint8_t* p2p_slot = s_p2p_slot;
+  const uint8_t* p2p_slot = p.p2p_bslot;  // advanced to the plan's boundaries below
   double* p2p_val = s_p2p_val;
   double* w_arr = s_w_arr;
   int32_t* w_i32 = s_w_i32;
   double* memo = s_memo;
-  double* tab = reinterpret_cast<double*>(smem_raw + L.tab);
+  // curves too large for the shared-memory budget stage into the unit's
+  // global region (host: Unit::gtab)
+  double* tab = U.gtab >= 0 ? p.g_tab + U.gtab : reinterpret_cast<double*>(smem_raw + L.tab);
 
   // ---- plan constants (warp-uniform) ----
   const int pl = U.plan;
@@ -401,8 +409,11 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
   __syncwarp();
 
-  // distinct p2p tables: boundaries only span 1 or 2 nodes in practice
+  // distinct p2p tables in first-appearance order (the host's bslot uses
+  // the same rule): boundaries only span 1 or 2 nodes in practice
+  p2p_slot += b0;
   int ND = 0;
+  uint64_t p2p_mask = 0;  // ND <= 2: bit b = distinct-curve slot of boundary b < 64
   for (int b = 0; b < NB; ++b) {
     const int t = p.p2p_tab[b0 + b];
     int s = 0;
@@ -413,12 +424,10 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       ++ND;
       __syncwarp();
     }
-    if (lane == 0) p2p_slot[b] = uint8_t(s);
+    if (s == 1 && b < 64) p2p_mask |= uint64_t(1) << b;
   }
   const int NQ = K + ND;  // curves: collectives, then distinct p2p
-  uint64_t p2p_mask = 0;  // ND <= 2: bit b = distinct-curve slot of boundary b
   __syncwarp();
-  for (int b = 0; b < NB && ND <= 2; ++b) p2p_mask |= uint64_t(p2p_slot[b]) << b;
   for (int i = lane; i < 4 * kMemoCap; i += kWarp) {
     memo[i] = -1.0;
     s_rkey[i] = 0ull;
@@ -427,23 +436,23 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     const int sig = p.cell_sig[size_t(U.fslot) * p.n_cells_total + c0 + lane];
     cellq[lane] = p.qoff[sig];
   }
-  if (lane < NQ) {
+  for (int q = lane; q < NQ; q += kWarp) {
     CurveDesc d;
-    if (lane < K) {
-      const int g = k0 + lane;
+    if (q < K) {
+      const int g = k0 + q;
       d.table = p.coll_tab[g];
       d.ppt = p.P.coll_ppt[g];
       d.share = p.P.coll_share[g];
       d.emul = double(p.P.coll_groups[g]);  // query_energy * groups_per_stage
     } else {
-      d.table = cdesc[lane].table;
+      d.table = cdesc[q].table;
       d.ppt = p2p_ppt;  // payload = p2p_ppt * tokens; x * 1.0 is exact
       d.share = 1.0;
       d.emul = 1.0;
     }
     d.n = d.table >= 0 ? p.S.k_n[d.table] : 1;
     d.hint = 0;
-    cdesc[lane] = d;
+    cdesc[q] = d;
   }
   __syncwarp();
   {  // stage the curves: knots[n] then (seconds, joules)[n] interleaved
@@ -468,6 +477,8 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   __syncwarp();
   EvalCtx ectx;
   ectx.qtab = qtab;
+  ectx.tab = tab;
+  ectx.bslot = p2p_slot;
   ectx.p2p_mask = p2p_mask;
   ectx.sdd = sdd;
   ectx.reps = reps;
@@ -989,7 +1000,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         for (int st = lane; st < S; st += kWarp) {
           double sec = srep, jou = jrep;  // stage s: block * reps, + p2p of boundary s-1
           if (st > 0 && st - 1 < NB) {
-            const int sl = p2p_slot[st - 1];
+            const int sl = __ldg(p2p_slot + st - 1);
             sec = __dadd_rn(srep, p2p_val[sl]);
             jou = __dadd_rn(jrep, p2p_val[kMaxClampSlots + sl]);
           }
@@ -1280,7 +1291,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
           p.slot_tpot[s] = __dsub_rn(clock, r_ft);  // / (gen - 1) in entry_reduce_kernel
           p.slot_status[s] = 1;
           r_fin = kDead;
-          tok = unsigned(r_ctx + r_gen);
+          tok = unsigned(r_ctx + (r_gen > 1 ? r_gen : 1));  // the ledger holds ctx + max(gen, 1)
         }
         const int64_t freed = int64_t(__reduce_add_sync(kFull, tok));
         const int nfin = __popc(__ballot_sync(kFull, fnow));
@@ -1311,7 +1322,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
             p.slot_tpot[s] = __dsub_rn(clock, ft);  // / (gen - 1) in entry_reduce_kernel
             p.slot_status[s] = 1;
             a.fin[i] = kDead;
-            tok = unsigned(a.ctx[i] + gen);
+            tok = unsigned(a.ctx[i] + (gen > 1 ? gen : 1));  // the ledger holds ctx + max(gen, 1)
           }
           freed += int64_t(__reduce_add_sync(kFull, tok));
           nfin += __popc(__ballot_sync(kFull, fnow));
@@ -1463,8 +1474,8 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       if (bits) atomicOr(p.clamp_compute + t, bits);
     }
   }
-  if (tot_hi >= 0 && lane < NQ) {
-    const CurveDesc& d = cdesc[lane];
+  for (int q = lane; tot_hi >= 0 && q < NQ; q += kWarp) {
+    const CurveDesc& d = cdesc[q];
     if (d.table >= 0) {
       const double xlo = __dmul_rn(__dmul_rn(d.ppt, double(tot_lo)), d.share);
       const double xhi = __dmul_rn(__dmul_rn(d.ppt, double(tot_hi)), d.share);
@@ -1476,7 +1487,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
 }
 
 // The speculation warp: prices posted jobs until the simulation warp quits.
-__device__ __noinline__ void spec_helper(const double* tab, const unsigned sleep_ns) {
+__device__ __noinline__ void spec_helper(const unsigned sleep_ns) {
   const int lane = threadIdx.x - kWarp;
   unsigned last = 0;
   while (true) {
@@ -1494,7 +1505,7 @@ __device__ __noinline__ void spec_helper(const double* tab, const unsigned sleep
     __threadfence_block();
     const EvalCtx E = s_spec.ctx;
     const EvalOut o = eval_iteration(
-        E, lane, [&](int) { return tok; }, 1, dec, dec + tok, s_cellq, s_cdesc, tab, s_p2p_slot,
+        E, lane, [&](int) { return tok; }, 1, dec, dec + tok, s_cellq, s_cdesc, E.tab, E.bslot,
         s_qv2, s_p2p_val2);
     if (lane == 0) {
       s_spec.cd = o.cd;
@@ -1536,9 +1547,7 @@ __device__ __forceinline__ void spec_block(const SimParams& p) {
   }
   __syncthreads();
   if (threadIdx.x >= kWarp) {  // the speculation warp
-    spec_helper(reinterpret_cast<const double*>(
-                    smem_raw + smem_layout(p.smem_cap, p.memo_cap, p.tab_smem, p.cm2_cap).tab),
-                unsigned(p.spec_sleep_ns));
+    spec_helper(unsigned(p.spec_sleep_ns));
     return;
   }
   sim_block<true, false, kMode>(p, smem_raw);

@@ -18,10 +18,7 @@
 
 namespace psg {
 
-__global__ void __launch_bounds__(256) qtab_kernel(const TabParams p) {
-  const int sig = blockIdx.x;
-  const int64_t tok = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
-  if (tok >= p.sig_rows[sig]) return;
+__device__ __forceinline__ void qtab_row(const TabParams& p, const int sig, const int64_t tok) {
   double* row = p.qtab + (p.qoff[sig] + tok) * 4;
   const int table = p.sig_table[sig];
   if (table < 0) {  // missing grid: never read (the entry fails at its first step)
@@ -40,10 +37,7 @@ __global__ void __launch_bounds__(256) qtab_kernel(const TabParams p) {
   row[3] = op_bytes(op, x, tasks, width, p.sig_hidden[sig], p.sig_kv[sig]);
 }
 
-__global__ void __launch_bounds__(256) dectab_kernel(const TabParams p) {
-  const int e = blockIdx.x;
-  const int64_t B = int64_t(blockIdx.y) * blockDim.x + threadIdx.x + 1;
-  if (B > p.ent_rows[e]) return;
+__device__ __forceinline__ void dectab_row(const TabParams& p, const int e, const int64_t B) {
   double* out = p.dectab + (p.doff[e] + B - 1) * 4;
   if (p.entry_missing[e]) {
     out[0] = out[1] = out[2] = out[3] = 0.0;
@@ -85,6 +79,20 @@ __global__ void __launch_bounds__(256) dectab_kernel(const TabParams p) {
   out[1] = E;
   out[2] = __dmul_rn(__dmul_rn(__dmul_rn(bf, sdd), reps), Sd);
   out[3] = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
+}
+
+__global__ void __launch_bounds__(256) qtab_kernel(const TabParams p) {
+  const int sig = blockIdx.x;
+  for (int64_t tok = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; tok < p.sig_rows[sig];
+       tok += int64_t(gridDim.y) * blockDim.x)
+    qtab_row(p, sig, tok);
+}
+
+__global__ void __launch_bounds__(256) dectab_kernel(const TabParams p) {
+  const int e = blockIdx.x;
+  for (int64_t B = int64_t(blockIdx.y) * blockDim.x + threadIdx.x + 1; B <= p.ent_rows[e];
+       B += int64_t(gridDim.y) * blockDim.x)
+    dectab_row(p, e, B);
 }
 
 }  // namespace psg

@@ -15,12 +15,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <set>
 #include <sstream>
+#include <thread>
 #include <tuple>
 
 #include "json.hpp"
@@ -32,28 +34,37 @@ namespace {
 
 using namespace plansim;
 
+// A cached engine context.  A psg_context is not thread-shared (psg.h), so
+// every use holds its mutex from psg_search until the results are copied out.
 struct Ctx {
   psg_context* h = nullptr;
+  std::mutex mu;
   ~Ctx() {
     if (h) psg_context_destroy(h);
   }
 };
 
-psg_context* context_for(int device) {
+// Context `slot` of `device` (slots > 0 only when several shards share a
+// device: PSG_SHIM_CONTEXTS_PER_DEVICE).
+Ctx& context_for(int device, int slot = 0) {
   static std::mutex mu;
-  static std::map<int, std::unique_ptr<Ctx>> ctxs;
+  static std::map<std::pair<int, int>, std::unique_ptr<Ctx>> ctxs;
   std::lock_guard<std::mutex> lock(mu);
-  auto& c = ctxs[device];
+  auto& c = ctxs[{device, slot}];
   if (!c) {
-    c = std::make_unique<Ctx>();
-    if (psg_context_create(device, &c->h) != PSG_OK) {
-      c.reset();
+    auto made = std::make_unique<Ctx>();
+    if (psg_context_create(device, &made->h) != PSG_OK)
       throw DataError("plansim_gpu: cannot create a CUDA context on device " +
                       std::to_string(device));
-    }
+    c = std::move(made);
   }
-  return c->h;
+  return *c;
 }
+
+struct ResultFree {
+  void operator()(psg_result* r) const { psg_result_free(r); }
+};
+using ResultPtr = std::unique_ptr<psg_result, ResultFree>;
 
 // Flat store tables parsed from ProfileStore::serialize().
 struct FlatStore {
@@ -233,6 +244,127 @@ struct FlatPlans {
 
 namespace {
 
+struct ShardFailed {};
+
+// SearchEntry k of a psg_result (report scalars, per-request metrics, rejected ids).
+void fill_entry(const psg_result& res, int64_t k, const std::vector<plansim::ExecutionPlan>& plans,
+                plansim::SearchEntry& se) {
+  using namespace plansim;
+  const psg_entry& e = res.entries[k];
+  se.plan_index = size_t(e.plan_index);
+  se.freq_ghz = e.freq_ghz;
+  SimulationReport& r = se.report;
+  r.plan_encoding = plans[size_t(e.plan_index)].scheme.encoding;
+  r.frequency_ghz = e.freq_ghz;
+  r.e2e_latency = e.e2e_latency;
+  r.total_energy = e.total_energy;
+  r.p95_latency = e.p95_latency;
+  r.mean_ttft = e.mean_ttft;
+  r.mean_tpot = e.mean_tpot;
+  r.mfu = e.mfu;
+  r.mbu = e.mbu;
+  r.num_completed = e.num_completed;
+  r.num_rejected = e.num_rejected;
+  r.num_iterations = e.num_iterations;
+  r.max_batch_observed = e.max_batch_observed;
+  static_assert(sizeof(RequestMetrics) == sizeof(psg_request_metrics), "layout");
+  r.per_request.resize(size_t(e.num_completed));
+  if (e.num_completed)
+    std::memcpy(r.per_request.data(), res.per_request + e.per_request_offset,
+                sizeof(RequestMetrics) * size_t(e.num_completed));
+  r.rejected_ids.assign(res.rejected_ids + e.rejected_offset,
+                        res.rejected_ids + e.rejected_offset + e.num_rejected);
+}
+
+// A ranked search over `shards` engine contexts (one per device, cycling over
+// the visible devices): entries are assigned longest-first (cost = requests
+// per DP replica, the length of the entry's serial chain), each shard runs
+// unranked on its own thread, and the gathered ranking records are ordered on
+// the first context's device with the reference comparator
+// (simulator.cpp:283-294; entry index breaks exact ties, as in one search).
+// Any shard error re-runs the search on one context, which reports the
+// reference's error for the lowest failing entry.
+plansim::RankedPlans run_sharded(const std::vector<plansim::ExecutionPlan>& plans,
+                                 const FlatPlans& fp, const FlatStore& fs,
+                                 const plansim::ProfileStore& store, const psg_cluster& cl,
+                                 const psg_trace& tr, const psg_config& base,
+                                 plansim::Objective objective, int device, int shards) {
+  using namespace plansim;
+  int ndev = 0;
+  if (psg_device_count(&ndev) != PSG_OK || ndev < 1) ndev = 1;
+  const int F = std::max(1, base.n_freqs);
+  const int64_t n_entries = int64_t(plans.size()) * F;
+  std::vector<std::pair<double, int32_t>> cost;
+  for (int64_t e = 0; e < n_entries; ++e)
+    cost.push_back({double(tr.n) / double(std::max(1, fp.v.model_dp[e / F])), int32_t(e)});
+  std::sort(cost.begin(), cost.end(),
+            [](const auto& a, const auto& b) { return a.first != b.first ? a.first > b.first : a.second < b.second; });
+  std::vector<double> load(static_cast<size_t>(shards), 0.0);
+  std::vector<std::vector<int32_t>> sub(static_cast<size_t>(shards));
+  for (const auto& [w, e] : cost) {
+    const size_t k = size_t(std::min_element(load.begin(), load.end()) - load.begin());
+    load[k] += w;
+    sub[k].push_back(e);
+  }
+  std::vector<ResultPtr> res(static_cast<size_t>(shards));
+  std::vector<int> rcs(static_cast<size_t>(shards), PSG_OK);
+  std::vector<std::thread> th;
+  for (int k = 0; k < shards; ++k) {
+    std::sort(sub[size_t(k)].begin(), sub[size_t(k)].end());
+    th.emplace_back([&, k] {
+      psg_config c = base;
+      c.rank = 0;
+      c.n_entry_subset = int32_t(sub[size_t(k)].size());
+      c.entry_subset = sub[size_t(k)].data();
+      try {
+        Ctx& cx = context_for((device + k) % ndev, k / ndev);
+        std::lock_guard<std::mutex> lock(cx.mu);
+        psg_result* raw = nullptr;
+        rcs[size_t(k)] = psg_search(cx.h, &fp.v, &cl, &fs.v, &tr, &c, &raw);
+        res[size_t(k)].reset(raw);
+      } catch (...) {
+        rcs[size_t(k)] = PSG_ERR_CUDA;
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int k = 0; k < shards; ++k)
+    if (rcs[size_t(k)] != PSG_OK) throw ShardFailed{};
+  std::vector<psg_rank_key> keys;
+  std::vector<std::pair<int, int64_t>> where;
+  const bool lat = objective == Objective::Latency;
+  for (int k = 0; k < shards; ++k) {
+    const psg_result& r = *res[size_t(k)];
+    fs.replay_clamps(store, r.compute_clamp, r.curve_clamp);
+    for (int64_t i = 0; i < r.n_entries; ++i) {
+      const psg_entry& e = r.entries[i];
+      psg_rank_key key{};
+      key.num_rejected = e.num_rejected;
+      key.objective_metric = lat ? e.e2e_latency : e.total_energy;
+      key.other_metric = lat ? e.total_energy : e.e2e_latency;
+      key.enc_rank = fp.v.enc_rank[e.plan_index];
+      key.freq_ghz = e.freq_ghz;
+      key.entry_index = e.entry_index;
+      keys.push_back(key);
+      where.push_back({k, i});
+    }
+  }
+  std::vector<int64_t> order(keys.size());
+  {
+    Ctx& cx = context_for(device % ndev, 0);
+    std::lock_guard<std::mutex> lock(cx.mu);
+    if (psg_rank_keys(cx.h, keys.data(), int64_t(keys.size()), order.data()) != PSG_OK)
+      throw DataError(psg_last_error(cx.h));
+  }
+  RankedPlans out;
+  out.entries.resize(keys.size());
+  for (size_t j = 0; j < order.size(); ++j) {
+    const auto& [k, i] = where[size_t(order[j])];
+    fill_entry(*res[size_t(k)], i, plans, out.entries[j]);
+  }
+  return out;
+}
+
 // One psg_search call.  subset / caps: optional repeated entry list with
 // per-entry max_batch_size (sweeps); emit: IterationRecords into the single
 // entry's report.
@@ -242,7 +374,7 @@ plansim::RankedPlans run(const std::vector<plansim::ExecutionPlan>& plans,
                          const std::vector<double>& frequencies, const plansim::SimConfig& cfg,
                          int device, bool rank, bool detail, bool emit,
                          const std::vector<int32_t>& subset = {},
-                         const std::vector<int64_t>& caps = {}) {
+                         const std::vector<int64_t>& caps = {}, int jobs = 1) {
   using namespace plansim;
   if (plans.empty()) throw InfeasibleError("search: no feasible plan");
   const FlatPlans fp(plans);
@@ -279,41 +411,35 @@ plansim::RankedPlans run(const std::vector<plansim::ExecutionPlan>& plans,
   c.entry_subset = subset.empty() ? nullptr : subset.data();
   c.entry_max_batch_size = caps.empty() ? nullptr : caps.data();
   c.emit_iterations = emit ? 1 : 0;
-  psg_context* h = context_for(device);
-  psg_result* res = nullptr;
-  const int rc = psg_search(h, &fp.v, &cl, &fs.v, &tr, &c, &res);
-  if (rc == PSG_ERR_INFEASIBLE) throw InfeasibleError(psg_last_error(h));
-  if (rc != PSG_OK) throw DataError(psg_last_error(h));
+  // jobs -> devices (simulator.cpp:251-275 maps jobs to worker threads):
+  // a ranked search with jobs > 1 shards its entries over the visible devices
+  int shards = 1;
+  if (rank && !emit && subset.empty() && caps.empty() && jobs > 1) {
+    int ndev = 0;
+    if (psg_device_count(&ndev) != PSG_OK || ndev < 1) ndev = 1;
+    int per = 1;
+    if (const char* e = std::getenv("PSG_SHIM_CONTEXTS_PER_DEVICE")) per = std::max(1, std::atoi(e));
+    const int64_t F = frequencies.empty() ? 1 : int64_t(frequencies.size());
+    shards = int(std::min<int64_t>({int64_t(jobs), int64_t(ndev) * per, int64_t(plans.size()) * F}));
+  }
+  if (shards > 1) {
+    try {
+      return run_sharded(plans, fp, fs, store, cl, tr, c, objective, device, shards);
+    } catch (const ShardFailed&) {  // the single-context search reports the error
+    }
+  }
+  Ctx& cx = context_for(device);
+  std::lock_guard<std::mutex> lock(cx.mu);
+  psg_result* raw = nullptr;
+  const int rc = psg_search(cx.h, &fp.v, &cl, &fs.v, &tr, &c, &raw);
+  ResultPtr res(raw);
+  if (rc == PSG_ERR_INFEASIBLE) throw InfeasibleError(psg_last_error(cx.h));
+  if (rc != PSG_OK) throw DataError(psg_last_error(cx.h));
   fs.replay_clamps(store, res->compute_clamp, res->curve_clamp);
   RankedPlans out;
   out.entries.resize(size_t(res->n_entries));
-  for (int64_t k = 0; k < res->n_entries; ++k) {
-    const psg_entry& e = res->entries[k];
-    SearchEntry& se = out.entries[size_t(k)];
-    se.plan_index = size_t(e.plan_index);
-    se.freq_ghz = e.freq_ghz;
-    SimulationReport& r = se.report;
-    r.plan_encoding = plans[size_t(e.plan_index)].scheme.encoding;
-    r.frequency_ghz = e.freq_ghz;
-    r.e2e_latency = e.e2e_latency;
-    r.total_energy = e.total_energy;
-    r.p95_latency = e.p95_latency;
-    r.mean_ttft = e.mean_ttft;
-    r.mean_tpot = e.mean_tpot;
-    r.mfu = e.mfu;
-    r.mbu = e.mbu;
-    r.num_completed = e.num_completed;
-    r.num_rejected = e.num_rejected;
-    r.num_iterations = e.num_iterations;
-    r.max_batch_observed = e.max_batch_observed;
-    static_assert(sizeof(RequestMetrics) == sizeof(psg_request_metrics), "layout");
-    r.per_request.resize(size_t(e.num_completed));
-    if (e.num_completed)
-      std::memcpy(r.per_request.data(), res->per_request + e.per_request_offset,
-                  sizeof(RequestMetrics) * size_t(e.num_completed));
-    r.rejected_ids.assign(res->rejected_ids + e.rejected_offset,
-                          res->rejected_ids + e.rejected_offset + e.num_rejected);
-  }
+  for (int64_t k = 0; k < res->n_entries; ++k)
+    fill_entry(*res, k, plans, out.entries[size_t(k)]);
   if (emit && res->n_iterations > 0) {  // simulator.cpp:158-170
     SimulationReport& r = out.entries.front().report;
     const int S = res->n_stages;
@@ -328,7 +454,6 @@ plansim::RankedPlans run(const std::vector<plansim::ExecutionPlan>& plans,
       it.stage_joules.assign(res->stage_joules + i * S, res->stage_joules + (i + 1) * S);
     }
   }
-  psg_result_free(res);
   return out;
 }
 
@@ -339,8 +464,9 @@ plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
                             const plansim::ClusterSpec& cluster, const plansim::Trace& trace,
                             const plansim::ProfileStore& store, plansim::Objective objective,
                             const std::vector<double>& frequencies,
-                            const plansim::SimConfig& cfg, int /*jobs*/, int device) {
-  return run(plans, cluster, trace, store, objective, frequencies, cfg, device, true, true, false);
+                            const plansim::SimConfig& cfg, int jobs, int device) {
+  return run(plans, cluster, trace, store, objective, frequencies, cfg, device, true, true, false,
+             {}, {}, jobs);
 }
 
 plansim::SimulationReport simulate_plan(const plansim::ExecutionPlan& plan,

@@ -17,8 +17,12 @@
 
 namespace plansim_gpu {
 
-// `jobs` is accepted for signature compatibility; the GPU is the worker pool.
-// `device` selects the CUDA device (one context per device is cached).
+// `jobs` maps to devices (the reference's worker threads,
+// simulator.cpp:251-275): with jobs > 1 the entries are sharded longest-first
+// over min(jobs, visible devices) contexts starting at `device` and ranked
+// together; the result is identical for every jobs value.  `device` selects
+// the (first) CUDA device; contexts are cached per device and locked per call,
+// so concurrent callers are safe.
 plansim::RankedPlans search(const std::vector<plansim::ExecutionPlan>& plans,
                             const plansim::ModelSpec& model,
                             const plansim::ClusterSpec& cluster,

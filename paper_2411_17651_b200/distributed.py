@@ -43,8 +43,9 @@ def lpt_shards(costs, n_problems, world):
     return shards
 
 
-def rank_keys_of(result, enc_rank, objective):
-    """psg_rank_key records of a (sharded, unranked) SearchResult."""
+def rank_keys_of(result, enc_rank, objective, slo=None):
+    """psg_rank_key records of a (sharded, unranked) SearchResult; `slo`: the
+    search's ttft_slo when SLO-constrained ranking is on."""
     ent = result.entries
     k = np.zeros(len(ent), dtype=abi.RANK_KEY_DTYPE)
     lat = objective == "latency"
@@ -54,6 +55,7 @@ def rank_keys_of(result, enc_rank, objective):
     k["enc_rank"] = [enc_rank[int(p)] for p in ent["plan_index"]]
     k["freq_ghz"] = ent["freq_ghz"]
     k["entry_index"] = ent["entry_index"]
+    k["slo_miss"] = (ent["slo_met"] == 0) if slo else 0
     return k
 
 

@@ -325,7 +325,8 @@ ANCHOR = {"arrival": 0, "admission": 1}
 class Config:
     def __init__(self, objective="latency", freqs=(), batching="contiguous", chunk_size=256,
                  max_batch_size=0, ttft_anchor="arrival", detail=True, rank=True,
-                 entry_subset=None, entry_max_batch_size=None, emit_iterations=False):
+                 entry_subset=None, entry_max_batch_size=None, emit_iterations=False,
+                 ttft_slo=0.0, slo_quantile=0.0):
         self.freqs = np.ascontiguousarray(list(freqs) or [0.0], dtype=np.float64)
         self.subset = np.ascontiguousarray(entry_subset if entry_subset is not None else [0],
                                            dtype=np.int32)
@@ -346,6 +347,9 @@ class Config:
         s.entry_max_batch_size = (self.caps.ctypes.data_as(C.POINTER(C.c_int64))
                                   if self.caps is not None else None)
         s.emit_iterations = int(bool(emit_iterations))
+        s.ttft_slo = float(ttft_slo)          # > 0: TTFT-SLO-constrained ranking
+        s.slo_quantile = float(slo_quantile)  # 0 => 0.99
         self.struct = s
         self.args = dict(objective=objective, batching=batching, chunk_size=chunk_size,
-                         max_batch_size=max_batch_size, ttft_anchor=ttft_anchor)
+                         max_batch_size=max_batch_size, ttft_anchor=ttft_anchor,
+                         ttft_slo=ttft_slo, slo_quantile=slo_quantile)

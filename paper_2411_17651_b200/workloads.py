@@ -97,7 +97,7 @@ class Workload:
     """One search problem: model + cluster + trace recipe + search options."""
 
     def __init__(self, key, title, model, cluster, trace, freqs=None,
-                 objective="latency", max_context=131072.0):
+                 objective="latency", max_context=131072.0, ttft_slo=0.0, slo_quantile=0.0):
         self.key = key
         self.title = title
         self.model = model          # dict
@@ -106,6 +106,8 @@ class Workload:
         self.freqs = freqs or []
         self.objective = objective
         self.max_context = max_context
+        self.ttft_slo = ttft_slo          # > 0: TTFT-SLO-constrained ranking (not in the reference)
+        self.slo_quantile = slo_quantile
 
     @property
     def model_json(self) -> str:
@@ -170,6 +172,10 @@ WORKLOADS = {
     "c3": Workload("c3", "GPT-3 175B, 4x8, 1188 summarization req, rate 2",
                    GPT3_175B, cluster_json(4),
                    ("synth", SUMMARIZATION + (2.0, 1188, 7))),
+    "c3slo": Workload("c3slo", "GPT-3 175B, 4x8, 1188 summarization req, rate 2: energy-optimal "
+                               "plans under a p99 TTFT SLO of 0.5 s, freqs {0.8,2.0}",
+                      GPT3_175B, cluster_json(4), ("synth", SUMMARIZATION + (2.0, 1188, 7)),
+                      freqs=[0.8, 2.0], objective="energy", ttft_slo=0.5, slo_quantile=0.99),
     "c4": Workload("c4", "Mixtral 8x7B, 1x8, 512 creation req, freqs {0.8,2.0}",
                    MIXTRAL_8X7B, cluster_json(None, leaf=8),
                    ("synth", CREATION + (1.0, 512, 9)), freqs=[0.8, 2.0]),
@@ -180,6 +186,14 @@ WORKLOADS = {
     "c5": Workload("c5", "1.05T MoE (128e top-8), 16x8, 100k mixed req, rate 10",
                    MOE_1T, cluster_json(16),
                    ("lognormal", (100000, 10.0, 5, [SUMMARIZATION, CREATION, CHAT]))),
+    "c5dvfs": Workload("c5dvfs", "1.05T MoE fp16, 16x8, 100k mixed req, DVFS {0.8,2.0}",
+                       MOE_1T, cluster_json(16),
+                       ("lognormal", (100000, 10.0, 5, [SUMMARIZATION, CREATION, CHAT])),
+                       freqs=[0.8, 2.0]),
+    "c5fp8dvfs": Workload("c5fp8dvfs", "1.05T MoE fp8, 16x8, 100k mixed req, DVFS {0.8,2.0}",
+                          _fp8(MOE_1T), cluster_json(16),
+                          ("lognormal", (100000, 10.0, 5, [SUMMARIZATION, CREATION, CHAT])),
+                          freqs=[0.8, 2.0]),
     "c5_10k": Workload("c5_10k", "1.05T MoE, 16x8, 10k mixed req",
                        MOE_1T, cluster_json(16),
                        ("lognormal", (10000, 10.0, 5, [SUMMARIZATION, CREATION, CHAT]))),

@@ -3,6 +3,7 @@ exact same inputs (plans / store / trace dumped by the reference itself) into
 the engine's SoA structures."""
 from __future__ import annotations
 
+import hashlib
 import os
 
 import numpy as np
@@ -18,7 +19,7 @@ EXACT_TALLY = ("mfu", "mbu")  # per-replica partial tallies
 
 
 class RefCase:
-    def __init__(self, key, workdir, extra=(), jobs=None, out_ranked=False):
+    def __init__(self, key, workdir, extra=(), jobs=None, out_ranked=False, digest=False):
         self.key = key
         w = WORKLOADS[key]
         d = os.path.join(workdir, key + "".join(str(x) for x in extra).replace("-", "_"))
@@ -33,6 +34,8 @@ class RefCase:
         args = ["search"] + w.refdrv_args(paths) + list(extra) + [
             "--jobs", jobs, "--out-result", self.dump, "--out-plans", self.plans_path,
             "--out-store", self.store_path, "--out-trace", self.trace_path]
+        if digest:  # per-request arrays as SHA-256 digests (C5-100k: 1.2 GB otherwise)
+            args.append("--digest")
         self.ranked_path = os.path.join(d, "ranked.json") if out_ranked else None
         if out_ranked:
             args += ["--out-ranked", self.ranked_path]
@@ -46,7 +49,8 @@ class RefCase:
         self.workload = w
 
     def config(self, **kw):
-        cfg = dict(objective=self.workload.objective, freqs=self.workload.freqs)
+        cfg = dict(objective=self.workload.objective, freqs=self.workload.freqs,
+                   ttft_slo=self.workload.ttft_slo, slo_quantile=self.workload.slo_quantile)
         cfg.update(kw)
         return Config(**cfg)
 
@@ -68,9 +72,18 @@ def compare_to_ref(res, ref, tally_rtol=0.0):
             elif gv != rv:
                 bad.append(f"rank {i} {e['encoding']}: {f} {gv!r} != {rv!r}")
         pr, rj = res.report(i)
-        if not np.array_equal(pr, e["per_request"]):
+        if "per_request_sha256" in e:  # digest dump
+            if (len(pr) != e["n_per_request"] or
+                    hashlib.sha256(np.ascontiguousarray(pr).tobytes()).hexdigest()
+                    != e["per_request_sha256"]):
+                bad.append(f"rank {i} {e['encoding']}: per_request digest differs")
+            if (len(rj) != e["n_rejected"] or
+                    hashlib.sha256(np.ascontiguousarray(rj).tobytes()).hexdigest()
+                    != e["rejected_sha256"]):
+                bad.append(f"rank {i} {e['encoding']}: rejected_ids digest differs")
+        elif not np.array_equal(pr, e["per_request"]):
             bad.append(f"rank {i} {e['encoding']}: per_request differs")
-        if not np.array_equal(rj, e["rejected"]):
+        if "rejected" in e and not np.array_equal(rj, e["rejected"]):
             bad.append(f"rank {i} {e['encoding']}: rejected_ids differ")
         if len(bad) > 20:
             break

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol(header):
 def test_version_and_struct_sizes():
     lib = abi.load_library()
     assert b"sm_100a" in lib.psg_version()
-    assert abi.ENTRY_DTYPE.itemsize == 160
+    assert abi.ENTRY_DTYPE.itemsize == 176
     assert abi.METRICS_DTYPE.itemsize == 40       # == plansim::RequestMetrics
     assert abi.RANK_KEY_DTYPE.itemsize == 48
 
@@ -53,3 +53,11 @@ def test_engine_refuses_without_library(tmp_path):
             abi.load_library(str(tmp_path / "missing.so"))
         finally:
             abi._lib = abi._lib_backup
+
+
+def test_config_struct_matches_the_header():
+    """psg_config's C layout (include/psg.h) as ctypes sees it: the SLO fields
+    close the struct after emit_iterations."""
+    names = [f[0] for f in abi.ConfigC._fields_]
+    assert names[-3:] == ["emit_iterations", "ttft_slo", "slo_quantile"]
+    assert C.sizeof(abi.ConfigC) == 96

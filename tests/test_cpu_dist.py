@@ -85,3 +85,56 @@ def test_lpt_shards_balance_and_cover():
     assert flat == list(range(8))
     loads = [sum(costs[e][0] for e in r[0]) for r in sh]
     assert max(loads) - min(loads) <= 10
+
+
+def _worker_spaces(rank, world, port, out_q):
+    """bench.py's strong-scaling step over two design spaces, one of which has
+    fewer entries than ranks: every rank still issues one all_gather per
+    design space (empty shards contribute zero records)."""
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in (repo, os.path.join(repo, "oracle"), os.path.join(repo, "tests")):
+        sys.path.insert(0, p)
+    import torch.distributed as dist
+    import catalog
+    import pyoracle
+    from paper_2411_17651_b200 import abi
+    from paper_2411_17651_b200.host import problem_for
+    from paper_2411_17651_b200.inputs import Config
+    from paper_2411_17651_b200.workloads import WORKLOADS
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    probs = [problem_for(WORKLOADS["c1"]), catalog.dp2_full().prob]
+    freqs, objs = [[], []], ["latency", "latency"]
+    shards = pd.lpt_shards(pd.entry_costs(probs, freqs), len(probs), world)[rank]
+    merged = []
+    for pi, prob in enumerate(probs):
+        if shards[pi]:
+            res = pyoracle.oracle_search(prob.plans, prob.cluster, prob.store, prob.trace,
+                                         Config(rank=False, entry_subset=shards[pi]))
+            keys = pd.rank_keys_of(res, prob.plans.struct.enc_rank, objs[pi])
+        else:
+            keys = abi.empty_rank_keys()
+        allk = pd.all_gather_keys(keys)
+        merged.append(list(allk[key_sort(allk)]["entry_index"]))
+    if rank == 0:
+        full = [list(pyoracle.oracle_search(p.plans, p.cluster, p.store, p.trace, Config())
+                     .entries["entry_index"]) for p in probs]
+        out_q.put((merged, full))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_three_rank_step_with_an_empty_shard_lines_up_its_collectives():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_spaces, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    merged, full = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    assert merged == full

@@ -26,8 +26,8 @@ def ref_dumps(workdir, tag, model, cluster, extra):
     rc, _, err = pyoracle.refdrv(["synth"] + args + ["--out-store", d + "/store.jsonl",
                                                       "--out-trace", d + "/trace.jsonl"])
     assert rc == 0, err
-    rc, _, err = pyoracle.refdrv(["search"] + args + ["--plans", "0:1000000",
-                                                       "--out-plans", d + "/plans.json", "--jobs", "2"])
+    rc, _, err = pyoracle.refdrv(["search"] + args + ["--plans", "0:1000000", "--no-search",
+                                                       "--out-plans", d + "/plans.json"])
     return d, rc, err
 
 
@@ -43,7 +43,7 @@ FIXTURE_PROBLEMS = {
 
 
 @needs_ref
-@pytest.mark.parametrize("key", ["c1", "c3", "c4", "c5_1k"])
+@pytest.mark.parametrize("key", ["c1", "c2", "c2fp8", "c3", "c4", "c5_1k", "c5", "c5fp8dvfs"])
 def test_workload_inputs_match_reference(workdir, key):
     w = WORKLOADS[key]
     prob = problem_for(w)

@@ -171,3 +171,27 @@ def test_nearest_rank_p95_rule():
         s = np.sort(pr["e2e"])
         rank = math.ceil(0.95 * len(s))
         assert r.entries[k]["p95_latency"] == s[min(len(s) - 1, max(rank, 1) - 1)]
+
+
+def test_oracle_slo_ranking_partitions_the_reference_order(workdir):
+    """The restatement's TTFT-SLO ranking (psg.h psg_config.ttft_slo) equals the
+    compiled reference's ranking stably partitioned by the nearest-rank p99
+    TTFT of the reference's own per-request outputs."""
+    import numpy as np
+    from harness import RefCase
+    case = RefCase("c3slo", workdir)
+    o = pyoracle.oracle_search(case.plans, case.cluster, case.store, case.trace, case.config())
+
+    def nearest(v, q):
+        v = np.sort(v)
+        rank = int(np.ceil(q * len(v)))
+        return v[min(len(v) - 1, rank - 1 if rank else 0)]
+    met = [len(e["per_request"]) > 0 and nearest(e["per_request"]["ttft"], 0.99) <= 0.5
+           for e in case.ref]
+    want = [case.ref[i]["encoding"] for i in range(len(met)) if met[i]] + \
+           [case.ref[i]["encoding"] for i in range(len(met)) if not met[i]]
+    want_f = [case.ref[i]["freq_ghz"] for i in range(len(met)) if met[i]] + \
+             [case.ref[i]["freq_ghz"] for i in range(len(met)) if not met[i]]
+    got = [case.plans.encodings[int(p)] for p in o.entries["plan_index"]]
+    assert got == want and list(o.entries["freq_ghz"]) == want_f
+    assert 0 < sum(met) < len(met)

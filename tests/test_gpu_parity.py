@@ -50,6 +50,20 @@ def test_c2_matches_reference(engine, workdir, key):
     assert not bad, "\n".join(bad)
 
 
+@pytest.mark.slow
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+def test_c5_100k_matches_reference(engine, workdir):
+    """The north-star configuration (BASELINE.json configs[4]): 1.05T MoE on a
+    16x8 cluster, 100k mixed requests, 301 plans.  Every entry's scalars and
+    rank bit for bit; per-request metrics and rejected ids by SHA-256 of their
+    bytes (the reference dump would be 1.2 GB)."""
+    case = RefCase("c5", workdir, digest=True)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
+    assert not bad, "\n".join(bad)
+    assert len(res) == 301 and res.total_iterations == case.line["plan_iterations"]
+
+
 KERNEL_MODES = [("0", "1"), ("1", "1"), ("0", "0"), ("1", "0")]  # (PSG_SPECULATE, PSG_CHAIN_REPLICAS)
 
 

@@ -81,3 +81,38 @@ def test_drop_in_simulate_plan_iterations_and_sweep(workdir, key, extra):
     assert rc == 0, (line, err)
     assert line["mismatches"] == 0, line
     assert line["iterations"] > 0 and line["sweep_rows"] > 0
+
+
+SHARDED = [
+    ("c4", "2", "2"),    # 140 entries over two contexts
+    ("c3", "4", "4"),    # 104 entries over four contexts
+    ("c4e", "8", "3"),   # more jobs than contexts: min(jobs, contexts)
+]
+
+
+@needs
+@pytest.mark.parametrize("key,jobs,per_dev", SHARDED, ids=[f"{k}-j{j}-c{c}" for k, j, c in SHARDED])
+def test_drop_in_jobs_shard_over_contexts(workdir, key, jobs, per_dev):
+    """jobs -> devices: entries sharded longest-first over several engine
+    contexts (here several on the one device of the box), merged by the device
+    ranking — the same RankedPlans as the reference's search with `jobs`
+    threads (simulator.cpp:251-275)."""
+    w = WORKLOADS[key]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shimj_" + key))) + ["--jobs", jobs]
+    env = dict(os.environ, PSG_SHIM_CONTEXTS_PER_DEVICE=per_dev)
+    p = subprocess.run([SHIM] + [str(a) for a in args], capture_output=True, text=True,
+                       timeout=900, env=env)
+    line = next((json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")), None)
+    assert p.returncode == 0, (line, p.stderr)
+    assert line["mismatches"] == 0, line
+
+
+@needs
+def test_drop_in_is_safe_for_concurrent_callers(workdir):
+    """Four threads call plansim_gpu::search at once (one cached context per
+    device, locked per call): each gets the single caller's result."""
+    w = WORKLOADS["c1"]
+    args = w.refdrv_args(w.materialize(os.path.join(workdir, "shimt"))) + ["--threads", "4"]
+    rc, line, err = run(args)
+    assert rc == 0, (line, err)
+    assert line["mismatches"] == 0, line
