@@ -202,6 +202,24 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& model, const B
                                                  const ClusterSpec& cluster,
                                                  const PlanOptions& opts = {},
                                                  Engine* engine = nullptr);
+// generate_plans straight into the engine's plan SoA: the plan kernels map,
+// finalize and compact the candidates on the device (psg_plan_emit) and the
+// search consumes that SoA as is — no ExecutionPlan objects on the host.
+// The same plans, in the same order, field for field (tests/test_gpu_planner.py).
+struct DevicePlanSet {
+  psg_plan_soa* soa = nullptr;          // library-owned (psg_plan_soa_free)
+  std::vector<std::string> encodings;   // per plan, scheme.encoding
+  DevicePlanSet() = default;
+  DevicePlanSet(const DevicePlanSet&) = delete;
+  DevicePlanSet& operator=(const DevicePlanSet&) = delete;
+  ~DevicePlanSet();
+  const psg_plan_set& view() const { return soa->set; }
+  size_t size() const { return encodings.size(); }
+};
+std::unique_ptr<DevicePlanSet> generate_plans_direct(const ModelSpec& model, const BlockSpec& block,
+                                                     const ClusterSpec& cluster,
+                                                     const PlanOptions& opts = {},
+                                                     Engine* engine = nullptr);
 ExecutionPlan build_plan(const ModelSpec& model, const BlockSpec& block,
                          const ClusterSpec& cluster, int model_dp, int num_stages,
                          const std::vector<CellChoice>& cells, const PlanOptions& opts = {});

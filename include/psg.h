@@ -334,6 +334,29 @@ typedef struct psg_plan_record {
   double coll_share[PSG_PLAN_MAX_COLLS];
 } psg_plan_record;
 
+/* Device-emitted plan set (generate_plans without host ExecutionPlans):
+   the plan kernels' feasible candidates, first occurrence of each encoding,
+   compacted on the device straight into the psg_plan_set SoA psg_search
+   consumes.  The host lists the candidate space (psg_plan_space) and per
+   candidate / choice the few values that are strings or CellScheme
+   constants on the host side. */
+typedef struct psg_plan_emit_in {
+  const uint8_t* keep;                /* [candidates] 1: first occurrence of its encoding */
+  const int32_t* enc_rank;            /* [candidates] rank of its encoding (std::string order) */
+  const int32_t* ch_op;               /* [choices] CellScheme::op (PSG_OP_*) */
+  const double* ch_tasks;             /* [choices] CellScheme::query_tasks */
+  const double* ch_width;             /* [choices] CellScheme::query_width */
+  const double* ch_scale;             /* [choices] CellScheme::token_scale */
+  int32_t compute_dtype;              /* ExecutionPlan::compute_dtype */
+  double payload_per_token;           /* p2p_payload_per_token == every collective's */
+  double shape_hidden, shape_head_dim, shape_kv_elems;  /* ExecutionPlan::op_shape */
+} psg_plan_emit_in;
+
+typedef struct psg_plan_soa {
+  psg_plan_set set;                   /* views into library-owned arrays */
+  const int64_t* candidate;           /* per plan: its candidate index (group_first order) */
+} psg_plan_soa;
+
 typedef struct psg_context psg_context;
 
 const char* psg_version(void);
@@ -355,6 +378,13 @@ int psg_synth_compute(psg_context* ctx, const psg_synth_grid* grid, double* seco
    stages - 1 boundary node counts at p2p_offset[g] ([n_groups + 1]). */
 int psg_plan_compute(psg_context* ctx, const psg_plan_space* space, psg_plan_record* records,
                      int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
+
+/* Maps, finalizes and compacts the candidate space on the device (the
+   kernels of psg_plan_compute plus plan_emit_kernel); *out is freed with
+   psg_plan_soa_free.  InfeasibleError (3) when no candidate is kept. */
+int psg_plan_emit(psg_context* ctx, const psg_plan_space* space, const psg_plan_emit_in* in,
+                  psg_plan_soa** out);
+void psg_plan_soa_free(psg_plan_soa* soa);
 
 /* Evaluate-all-plans: plansim::search semantics (see header comment). */
 int psg_search(psg_context* ctx, const psg_plan_set* plans,

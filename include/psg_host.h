@@ -49,6 +49,10 @@ int psgh_trace_load(psgh_problem* p, const char* jsonl);
 int psgh_plans_generate(psgh_problem* p);
 /* The same plans with the candidates mapped and finalized on the GPU. */
 int psgh_plans_generate_device(psgh_problem* p);
+/* The same plans emitted by the device straight into the engine's plan SoA
+   (psg_plan_emit): no ExecutionPlans on the host; plans_view / count /
+   encoding serve it, plans_json and plan_build refuse it. */
+int psgh_plans_generate_direct(psgh_problem* p);
 /* build_plan(): appends one plan; modes[i] is 0 (TP) or 1 (EP). */
 int psgh_plan_build(psgh_problem* p, int model_dp, int num_stages, int n_cells,
                     const int32_t* modes, const int32_t* cell_dp, const int32_t* intra);

@@ -14,6 +14,7 @@ struct psgh_problem {
   psb::Trace trace;
   std::vector<psb::ExecutionPlan> plans;
   std::unique_ptr<psb::PlanSoA> soa;
+  std::unique_ptr<psb::DevicePlanSet> direct;  // generate_plans_direct: SoA only, no ExecutionPlans
   psg_cluster cl{};
   // trace SoA
   std::vector<int64_t> t_id, t_ctx, t_gen;
@@ -136,12 +137,22 @@ int psgh_plans_generate(psgh_problem* p) {
   return guarded([&] {
     p->plans = psb::generate_plans(p->model, p->block, p->cluster, p->opts);
     p->soa.reset();
+    p->direct.reset();
   });
 }
 
 int psgh_plans_generate_device(psgh_problem* p) {
   return guarded([&] {
     p->plans = psb::generate_plans_device(p->model, p->block, p->cluster, p->opts);
+    p->soa.reset();
+    p->direct.reset();
+  });
+}
+
+int psgh_plans_generate_direct(psgh_problem* p) {
+  return guarded([&] {
+    p->direct = psb::generate_plans_direct(p->model, p->block, p->cluster, p->opts);
+    p->plans.clear();
     p->soa.reset();
   });
 }
@@ -152,18 +163,22 @@ int psgh_plan_build(psgh_problem* p, int dp, int stages, int n_cells, const int3
     std::vector<psb::CellChoice> ch(static_cast<size_t>(n_cells));
     for (int i = 0; i < n_cells; ++i)
       ch[size_t(i)] = {modes[i] ? psb::ParallelMode::EP : psb::ParallelMode::TP, cell_dp[i], intra[i]};
+    if (p->direct) throw psb::DataError("build_plan: the problem holds a device-emitted plan set");
     p->plans.push_back(psb::build_plan(p->model, p->block, p->cluster, dp, stages, ch, p->opts));
     p->soa.reset();
   });
 }
 
-int psgh_plans_count(const psgh_problem* p) { return int(p->plans.size()); }
+int psgh_plans_count(const psgh_problem* p) {
+  return int(p->direct ? p->direct->size() : p->plans.size());
+}
 
 const char* psgh_plan_encoding(const psgh_problem* p, int i) {
-  return p->plans[size_t(i)].scheme.encoding.c_str();
+  return p->direct ? p->direct->encodings[size_t(i)].c_str() : p->plans[size_t(i)].scheme.encoding.c_str();
 }
 
 const psg_plan_set* psgh_plans_view(psgh_problem* p) {
+  if (p->direct) return &p->direct->view();
   if (!p->soa) p->soa = std::make_unique<psb::PlanSoA>(p->plans);
   return &p->soa->view();
 }
@@ -177,7 +192,13 @@ const psg_trace* psgh_trace_view(psgh_problem* p) {
 
 const psg_cluster* psgh_cluster_view(const psgh_problem* p) { return &p->cl; }
 
-char* psgh_plans_json(const psgh_problem* p) { return dup(psb::plans_to_json(p->plans)); }
+char* psgh_plans_json(const psgh_problem* p) {
+  if (p->direct) {
+    g_err = "plans_json: a device-emitted plan set has no ExecutionPlans";
+    return nullptr;
+  }
+  return dup(psb::plans_to_json(p->plans));
+}
 char* psgh_store_serialize(const psgh_problem* p) { return dup(p->store.serialize()); }
 char* psgh_trace_serialize(const psgh_problem* p) { return dup(psb::serialize_trace(p->trace)); }
 void psgh_string_free(char* s) { std::free(s); }

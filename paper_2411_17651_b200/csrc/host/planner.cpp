@@ -286,20 +286,31 @@ std::vector<ExecutionPlan> generate_plans(const ModelSpec& m, const BlockSpec& b
   return plans;
 }
 
-std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const BlockSpec& block,
-                                                 const ClusterSpec& cl, const PlanOptions& opts,
-                                                 Engine* engine) {
-  // Candidate groups and per-cell choices exactly as enumerate_schemes lists
-  // them; the device maps every group and finalizes every candidate.
-  const int n = cl.total_devices();
-  const int nc = int(block.cells.size());
-  if (nc < 1 || nc > PSG_PLAN_MAX_CELLS) throw DataError("plan space: unsupported cell count");
+namespace {
+
+// The candidate space generate_plans enumerates (groups in enumerate_schemes
+// order, per-cell scheme choices, last cell fastest) flattened for the plan
+// kernels (psg_plan_space), with the storage its pointers refer to.
+struct PlanSpace {
   struct Group {
     int dp, stages, sdev;
     std::vector<std::vector<CellScheme>> choices;
     long long combos;
   };
   std::vector<Group> groups;
+  std::vector<int32_t> subtree, att, gdp, gst, gsd, grp, cb, cm, cd, ci_;
+  std::vector<double> kvh, hd, cw;
+  std::vector<int64_t> gfirst{0}, p2p_off{0};
+  psg_plan_space sp{};
+};
+
+void build_space(const ModelSpec& m, const BlockSpec& block, const ClusterSpec& cl,
+                 const PlanOptions& opts, PlanSpace& S) {
+  const int n = cl.total_devices();
+  const int nc = int(block.cells.size());
+  if (nc < 1 || nc > PSG_PLAN_MAX_CELLS) throw DataError("plan space: unsupported cell count");
+  using Group = PlanSpace::Group;
+  std::vector<Group>& groups = S.groups;
   if (n >= 1 && block.repeat_count >= 1) {
     for (const int dp : divisors(n)) {
       const int per_replica = n / dp;
@@ -330,10 +341,18 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const Block
     }
   }
   const int G = int(groups.size());
-  std::vector<int32_t> subtree(static_cast<size_t>(cl.num_levels()) + 1), att(static_cast<size_t>(nc)),
-      gdp, gst, gsd, grp, cb, cm, cd, ci_;
-  std::vector<double> kvh(static_cast<size_t>(nc)), hd(static_cast<size_t>(nc)), cw;
-  std::vector<int64_t> gfirst{0}, p2p_off{0};
+  auto& subtree = S.subtree;
+  auto& att = S.att;
+  auto& kvh = S.kvh;
+  auto& hd = S.hd;
+  auto &gdp = S.gdp, &gst = S.gst, &gsd = S.gsd, &grp = S.grp, &cb = S.cb, &cm = S.cm, &cd = S.cd,
+       &ci_ = S.ci_;
+  auto& cw = S.cw;
+  auto &gfirst = S.gfirst, &p2p_off = S.p2p_off;
+  subtree.resize(static_cast<size_t>(cl.num_levels()) + 1);
+  att.resize(static_cast<size_t>(nc));
+  kvh.resize(static_cast<size_t>(nc));
+  hd.resize(static_cast<size_t>(nc));
   for (int l = 0; l <= cl.num_levels(); ++l) subtree[size_t(l)] = cl.subtree_capacity(l);
   for (int i = 0; i < nc; ++i) {
     att[size_t(i)] = block.cells[size_t(i)].is_attention() ? 1 : 0;
@@ -358,7 +377,7 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const Block
     }
   }
   cb.push_back(int32_t(cm.size()));
-  psg_plan_space sp{};
+  psg_plan_space& sp = S.sp;
   sp.n_devices = n;
   sp.per_node = cl.devices_per_node();
   sp.n_levels = cl.num_levels();
@@ -384,6 +403,24 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const Block
   sp.ch_cdp = cd.data();
   sp.ch_intra = ci_.data();
   sp.ch_weight = cw.data();
+}
+
+}  // namespace
+
+std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const BlockSpec& block,
+                                                 const ClusterSpec& cl, const PlanOptions& opts,
+                                                 Engine* engine) {
+  // Candidate groups and per-cell choices exactly as enumerate_schemes lists
+  // them; the device maps every group and finalizes every candidate.
+  PlanSpace S;
+  build_space(m, block, cl, opts, S);
+  const int n = cl.total_devices();
+  const int nc = int(block.cells.size());
+  const int G = int(S.groups.size());
+  const auto& groups = S.groups;
+  const auto& gfirst = S.gfirst;
+  const auto& p2p_off = S.p2p_off;
+  psg_plan_space& sp = S.sp;
   std::vector<psg_plan_record> rec(static_cast<size_t>(std::max<int64_t>(gfirst.back(), 1)));
   std::vector<int32_t> phys(static_cast<size_t>(std::max(G, 1)) * static_cast<size_t>(n));
   std::vector<int32_t> p2p(static_cast<size_t>(std::max<int64_t>(p2p_off.back(), 1)));
@@ -400,7 +437,7 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const Block
   std::set<std::string> seen;
   const double per_token = double(m.hidden_size) * m.activation_dtype.bytes_per_element;
   for (int gi = 0; gi < G; ++gi) {
-    const Group& g = groups[size_t(gi)];
+    const PlanSpace::Group& g = groups[size_t(gi)];
     std::vector<size_t> digit(static_cast<size_t>(nc), 0);
     for (long long k = 0; k < g.combos; ++k) {
       std::vector<CellScheme> cells;
@@ -443,6 +480,97 @@ std::vector<ExecutionPlan> generate_plans_device(const ModelSpec& m, const Block
   }
   if (plans.empty()) throw InfeasibleError("no parallel execution plan fits the model on this cluster");
   return plans;
+}
+
+DevicePlanSet::~DevicePlanSet() {
+  if (soa) psg_plan_soa_free(soa);
+}
+
+std::unique_ptr<DevicePlanSet> generate_plans_direct(const ModelSpec& m, const BlockSpec& block,
+                                                     const ClusterSpec& cl, const PlanOptions& opts,
+                                                     Engine* engine) {
+  PlanSpace S;
+  build_space(m, block, cl, opts, S);
+  const int nc = int(block.cells.size());
+  const int64_t total = S.gfirst.back();
+  // host-side per candidate: its encoding (assemble's format, planner.cpp:111-129
+  // here) -> first-occurrence flag and rank; per choice: the CellScheme query
+  // constants, in build_space's choice order
+  std::vector<std::string> enc(static_cast<size_t>(total));
+  std::vector<int32_t> ch_op;
+  std::vector<double> ch_t, ch_w, ch_s;
+  int64_t k0 = 0;
+  for (const auto& g : S.groups) {
+    for (const auto& opts_c : g.choices)
+      for (const CellScheme& c : opts_c) {
+        ch_op.push_back(int32_t(c.op));
+        ch_t.push_back(c.query_tasks);
+        ch_w.push_back(c.query_width);
+        ch_s.push_back(c.token_scale);
+      }
+    std::vector<size_t> digit(static_cast<size_t>(nc), 0);
+    for (long long k = 0; k < g.combos; ++k) {
+      std::string e = "dp" + std::to_string(g.dp) + ":pp" + std::to_string(g.stages);
+      for (int c = 0; c < nc; ++c) {
+        const CellScheme& cs = g.choices[size_t(c)][digit[size_t(c)]];
+        e += ":";
+        e += cell_kind_str(cs.cell.kind);
+        e += cs.mode == ParallelMode::EP ? "-ep" : "-tp";
+        e += std::to_string(cs.intra_degree) + "x" + std::to_string(cs.cell_dp);
+      }
+      enc[size_t(k0 + k)] = std::move(e);
+      for (size_t c = digit.size(); c-- > 0;) {
+        if (++digit[c] < g.choices[c].size()) break;
+        digit[c] = 0;
+      }
+    }
+    k0 += g.combos;
+  }
+  std::vector<uint8_t> keep(static_cast<size_t>(std::max<int64_t>(total, 1)), 0);
+  std::vector<int32_t> rank(static_cast<size_t>(std::max<int64_t>(total, 1)), 0);
+  {
+    std::vector<std::string> uniq(enc);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    std::set<std::string> seen;
+    for (int64_t k = 0; k < total; ++k) {
+      keep[size_t(k)] = seen.insert(enc[size_t(k)]).second ? 1 : 0;
+      rank[size_t(k)] = int32_t(std::lower_bound(uniq.begin(), uniq.end(), enc[size_t(k)]) - uniq.begin());
+    }
+  }
+  psg_plan_emit_in in{};
+  in.keep = keep.data();
+  in.enc_rank = rank.data();
+  in.ch_op = ch_op.empty() ? nullptr : ch_op.data();
+  in.ch_tasks = ch_t.empty() ? nullptr : ch_t.data();
+  in.ch_width = ch_w.empty() ? nullptr : ch_w.data();
+  in.ch_scale = ch_s.empty() ? nullptr : ch_s.data();
+  in.compute_dtype = int32_t(m.activation_dtype.name);
+  in.payload_per_token = double(m.hidden_size) * m.activation_dtype.bytes_per_element;
+  in.shape_hidden = m.hidden_size;
+  in.shape_head_dim = m.head_dim;
+  in.shape_kv_elems = 2.0 * m.head_dim / (m.num_attention_heads / double(m.num_kv_heads));
+  std::unique_ptr<Engine> own;
+  if (!engine) {
+    own = std::make_unique<Engine>(0);
+    engine = own.get();
+  }
+  auto out = std::make_unique<DevicePlanSet>();
+  const int rc = total > 0 ? psg_plan_emit(engine->handle(), &S.sp, &in, &out->soa) : PSG_ERR_INFEASIBLE;
+  if (rc == PSG_ERR_INFEASIBLE)
+    throw InfeasibleError("no parallel execution plan fits the model on this cluster");
+  if (rc != PSG_OK) throw DataError(std::string("plan space on device: ") + psg_last_error(engine->handle()));
+  for (int i = 0; i < out->soa->set.n_plans; ++i) out->encodings.push_back(enc[size_t(out->soa->candidate[i])]);
+  // the device wrote ranks among every candidate's encoding; PlanSoA ranks
+  // among the plans kept (the same order, other integers): use those, so the
+  // two plan sets are identical array for array
+  std::vector<std::string> uniq(out->encodings);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  auto* er = const_cast<int32_t*>(out->soa->set.enc_rank);  // library-owned host array
+  for (size_t i = 0; i < out->encodings.size(); ++i)
+    er[i] = int32_t(std::lower_bound(uniq.begin(), uniq.end(), out->encodings[i]) - uniq.begin());
+  return out;
 }
 
 ExecutionPlan build_plan(const ModelSpec& m, const BlockSpec& block, const ClusterSpec& cl,

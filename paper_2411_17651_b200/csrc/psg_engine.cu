@@ -254,13 +254,21 @@ int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* rec
   return guarded(ctx, [&] { return plan_compute_impl(ctx, s, records, phys, p2p_offset, p2p); });
 }
 
-static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
-                             int32_t* phys, const int64_t* p2p_offset, int32_t* p2p) {
-  if (!ctx || !s || !records || !phys || !p2p_offset || !p2p) return PSG_ERR_USAGE;
+// Uploads the plan space and runs plan_map_kernel + plan_candidate_kernel;
+// the records / assignments / boundary node counts stay on the device.
+struct PlanDev {
+  psg_plan_space ds;
+  psg_plan_record* rec;
+  int32_t *phys, *p2p;
+  const int64_t* p2p_off;
+  size_t end;  // first free byte of ctx->d_plan after the plan buffers
+};
+
+static int plan_device(psg_context* ctx, const psg_plan_space* s, const int64_t* p2p_offset,
+                       size_t extra, PlanDev& pd) {
   const int n = s->n_devices, G = s->n_groups, nc = s->n_cells;
   if (n < 1 || G < 0 || nc < 1 || nc > PSG_PLAN_MAX_CELLS || s->n_levels < 1)
     return fail(ctx, PSG_ERR_USAGE, "plan space: bad sizes");
-  if (G == 0) return PSG_OK;
   const int64_t total = s->group_first[G];
   const int64_t n_choice = s->choice_begin[int64_t(G) * nc];
   const int64_t n_p2p = p2p_offset[G];
@@ -278,19 +286,20 @@ static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan
                o_cw = pk.add(s->ch_weight, size_t(n_choice)), o_p2o = pk.add(p2p_offset, size_t(G) + 1);
   const size_t in_bytes = (pk.size + 15) & ~size_t(15);
   const size_t rec_bytes = sizeof(psg_plan_record) * size_t(std::max<int64_t>(total, 1));
-  const size_t phys_bytes = sizeof(int32_t) * size_t(G) * n;
+  const size_t phys_bytes = sizeof(int32_t) * size_t(std::max(G, 1)) * n;
   const size_t p2p_bytes = sizeof(int32_t) * size_t(std::max<int64_t>(n_p2p, 1));
-  const size_t span_bytes = sizeof(int32_t) * size_t(G) * (n + 1);
+  const size_t span_bytes = sizeof(int32_t) * size_t(std::max(G, 1)) * (n + 1);
   const size_t o_rec = in_bytes, o_phys = o_rec + ((rec_bytes + 15) & ~size_t(15)),
                o_p2p = o_phys + ((phys_bytes + 15) & ~size_t(15)),
                o_sn = o_p2p + ((p2p_bytes + 15) & ~size_t(15)),
-               o_sl = o_sn + ((span_bytes + 15) & ~size_t(15)), tot = o_sl + span_bytes;
-  PSG_CUDA(ctx->d_plan.ensure(tot));
+               o_sl = o_sn + ((span_bytes + 15) & ~size_t(15)), tot = o_sl + ((span_bytes + 15) & ~size_t(15));
+  PSG_CUDA(ctx->d_plan.ensure(tot + extra));
   PSG_CUDA(ctx->h_in.ensure(in_bytes));
   pk.write(static_cast<unsigned char*>(ctx->h_in.p));
   auto* d = static_cast<unsigned char*>(ctx->d_plan.p);
   PSG_CUDA(cudaMemcpyAsync(d, ctx->h_in.p, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  psg_plan_space ds = *s;
+  psg_plan_space& ds = pd.ds;
+  ds = *s;
   ds.subtree_cap = reinterpret_cast<const int32_t*>(d + o_cap);
   ds.cell_is_attention = reinterpret_cast<const int32_t*>(d + o_att);
   ds.cell_kv_heads = reinterpret_cast<const double*>(d + o_kvh);
@@ -305,28 +314,159 @@ static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan
   ds.ch_cdp = reinterpret_cast<const int32_t*>(d + o_cd);
   ds.ch_intra = reinterpret_cast<const int32_t*>(d + o_ci);
   ds.ch_weight = reinterpret_cast<const double*>(d + o_cw);
-  auto* d_rec = reinterpret_cast<psg_plan_record*>(d + o_rec);
-  auto* d_phys = reinterpret_cast<int32_t*>(d + o_phys);
-  auto* d_p2p = reinterpret_cast<int32_t*>(d + o_p2p);
+  pd.rec = reinterpret_cast<psg_plan_record*>(d + o_rec);
+  pd.phys = reinterpret_cast<int32_t*>(d + o_phys);
+  pd.p2p = reinterpret_cast<int32_t*>(d + o_p2p);
+  pd.p2p_off = reinterpret_cast<const int64_t*>(d + o_p2o);
+  pd.end = tot;
+  if (G == 0) return PSG_OK;
   auto* d_sn = reinterpret_cast<int32_t*>(d + o_sn);
   auto* d_sl = reinterpret_cast<int32_t*>(d + o_sl);
   if (map_smem > 48 * 1024)
     PSG_CUDA(cudaFuncSetAttribute(plan_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(map_smem)));
-  plan_map_kernel<<<G, 128, map_smem, ctx->stream>>>(ds, d_phys, reinterpret_cast<const int64_t*>(d + o_p2o),
-                                                     d_p2p, d_sn, d_sl);
+  plan_map_kernel<<<G, 128, map_smem, ctx->stream>>>(ds, pd.phys, pd.p2p_off, pd.p2p, d_sn, d_sl);
   PSG_CUDA(cudaGetLastError());
   if (total > 0) {
-    plan_candidate_kernel<<<unsigned((total + 127) / 128), 128, 0, ctx->stream>>>(ds, d_sn, d_rec);
+    plan_candidate_kernel<<<unsigned((total + 127) / 128), 128, 0, ctx->stream>>>(ds, d_sn, pd.rec);
     PSG_CUDA(cudaGetLastError());
-    PSG_CUDA(cudaMemcpyAsync(records, d_rec, sizeof(psg_plan_record) * size_t(total), cudaMemcpyDeviceToHost,
-                             ctx->stream));
   }
-  PSG_CUDA(cudaMemcpyAsync(phys, d_phys, phys_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return PSG_OK;
+}
+
+static int plan_compute_impl(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
+                             int32_t* phys, const int64_t* p2p_offset, int32_t* p2p) {
+  if (!ctx || !s || !records || !phys || !p2p_offset || !p2p) return PSG_ERR_USAGE;
+  if (s->n_groups == 0) return PSG_OK;
+  PlanDev pd{};
+  if (const int rc = plan_device(ctx, s, p2p_offset, 0, pd)) return rc;
+  const int G = s->n_groups;
+  const int64_t total = s->group_first[G], n_p2p = p2p_offset[G];
+  if (total > 0)
+    PSG_CUDA(cudaMemcpyAsync(records, pd.rec, sizeof(psg_plan_record) * size_t(total), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  PSG_CUDA(cudaMemcpyAsync(phys, pd.phys, sizeof(int32_t) * size_t(G) * s->n_devices, cudaMemcpyDeviceToHost,
+                           ctx->stream));
   if (n_p2p > 0)
-    PSG_CUDA(cudaMemcpyAsync(p2p, d_p2p, sizeof(int32_t) * size_t(n_p2p), cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(p2p, pd.p2p, sizeof(int32_t) * size_t(n_p2p), cudaMemcpyDeviceToHost, ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   return PSG_OK;
 }
+
+// The owned arrays behind a psg_plan_soa.
+struct PlanSoaOwned : psg_plan_soa {
+  std::vector<int32_t> dp, st, sd, reps, dt, enc, cb, cop, kb, kk, kd, kn, kg, pb, pn;
+  std::vector<double> kv, bud, ppt, hid, head, kve, ct, cw, cs, kp, ksh;
+  std::vector<int64_t> cand;
+};
+
+static int plan_emit_impl(psg_context* ctx, const psg_plan_space* s, const psg_plan_emit_in* in,
+                          psg_plan_soa** out) {
+  if (!ctx || !s || !in || !out) return PSG_ERR_USAGE;
+  *out = nullptr;
+  const int G = s->n_groups, nc = s->n_cells;
+  if (G < 1) return fail(ctx, PSG_ERR_INFEASIBLE, "no parallel execution plan fits the model on this cluster");
+  const int64_t total = s->group_first[G];
+  const int64_t n_choice = s->choice_begin[int64_t(G) * nc];
+  std::vector<int64_t> p2p_off(size_t(G) + 1, 0);
+  int64_t max_p2p = 0;  // boundaries of every candidate (upper bound of the kept ones)
+  for (int g = 0; g < G; ++g) {
+    p2p_off[size_t(g) + 1] = p2p_off[size_t(g)] + (s->group_stages[g] - 1);
+    max_p2p += (s->group_first[g + 1] - s->group_first[g]) * (s->group_stages[g] - 1);
+  }
+  // host inputs of the emission, then the output arrays (one region)
+  Packer pk;
+  const size_t o_keep = pk.add(in->keep, size_t(total)), o_enc = pk.add(in->enc_rank, size_t(total)),
+               o_op = pk.add(in->ch_op, size_t(n_choice)), o_t = pk.add(in->ch_tasks, size_t(n_choice)),
+               o_w = pk.add(in->ch_width, size_t(n_choice)), o_sc = pk.add(in->ch_scale, size_t(n_choice));
+  const size_t in_bytes = (pk.size + 15) & ~size_t(15);
+  Packer ok;  // offsets only
+  const size_t T = size_t(std::max<int64_t>(total, 1)), TC = T * size_t(nc),
+               TK = T * PSG_PLAN_MAX_COLLS, TP = size_t(std::max<int64_t>(max_p2p, 1));
+  const size_t w_dp = ok.add<int32_t>(nullptr, T), w_st = ok.add<int32_t>(nullptr, T),
+               w_sd = ok.add<int32_t>(nullptr, T), w_rp = ok.add<int32_t>(nullptr, T),
+               w_dt = ok.add<int32_t>(nullptr, T), w_en = ok.add<int32_t>(nullptr, T),
+               w_kv = ok.add<double>(nullptr, T), w_bu = ok.add<double>(nullptr, T),
+               w_pp = ok.add<double>(nullptr, T), w_hi = ok.add<double>(nullptr, T),
+               w_he = ok.add<double>(nullptr, T), w_ke = ok.add<double>(nullptr, T),
+               w_cb = ok.add<int32_t>(nullptr, T + 1), w_co = ok.add<int32_t>(nullptr, TC),
+               w_ct = ok.add<double>(nullptr, TC), w_cw = ok.add<double>(nullptr, TC),
+               w_cs = ok.add<double>(nullptr, TC), w_kb = ok.add<int32_t>(nullptr, T + 1),
+               w_kk = ok.add<int32_t>(nullptr, TK), w_kd = ok.add<int32_t>(nullptr, TK),
+               w_kn = ok.add<int32_t>(nullptr, TK), w_kg = ok.add<int32_t>(nullptr, TK),
+               w_kp = ok.add<double>(nullptr, TK), w_ks = ok.add<double>(nullptr, TK),
+               w_pb = ok.add<int32_t>(nullptr, T + 1), w_pn = ok.add<int32_t>(nullptr, TP),
+               w_ca = ok.add<int64_t>(nullptr, T), w_cnt = ok.add<int32_t>(nullptr, 4);
+  PlanDev pd{};
+  if (const int rc = plan_device(ctx, s, p2p_off.data(), in_bytes + ok.size + 64, pd)) return rc;
+  auto* base = static_cast<unsigned char*>(ctx->d_plan.p) + ((pd.end + 15) & ~size_t(15));
+  PSG_CUDA(ctx->h_in.ensure(in_bytes));
+  pk.write(static_cast<unsigned char*>(ctx->h_in.p));
+  PSG_CUDA(cudaMemcpyAsync(base, ctx->h_in.p, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  unsigned char* w = base + in_bytes;
+  auto W = [&](size_t o) { return static_cast<void*>(w + o); };
+  PlanEmitArgs a{};
+  a.keep = reinterpret_cast<const uint8_t*>(base + o_keep);
+  a.enc_rank = reinterpret_cast<const int32_t*>(base + o_enc);
+  a.ch_op = reinterpret_cast<const int32_t*>(base + o_op);
+  a.ch_tasks = reinterpret_cast<const double*>(base + o_t);
+  a.ch_width = reinterpret_cast<const double*>(base + o_w);
+  a.ch_scale = reinterpret_cast<const double*>(base + o_sc);
+  a.p2p_off = pd.p2p_off;
+  a.p2p = pd.p2p;
+  a.compute_dtype = in->compute_dtype;
+  a.payload_per_token = in->payload_per_token;
+  a.shape_hidden = in->shape_hidden;
+  a.shape_head_dim = in->shape_head_dim;
+  a.shape_kv_elems = in->shape_kv_elems;
+  PlanEmitOut o{(int32_t*)W(w_dp), (int32_t*)W(w_st), (int32_t*)W(w_sd), (int32_t*)W(w_rp),
+                (int32_t*)W(w_dt), (int32_t*)W(w_en), (double*)W(w_kv), (double*)W(w_bu),
+                (double*)W(w_pp), (double*)W(w_hi), (double*)W(w_he), (double*)W(w_ke),
+                (int32_t*)W(w_cb), (int32_t*)W(w_co), (double*)W(w_ct), (double*)W(w_cw),
+                (double*)W(w_cs), (int32_t*)W(w_kb), (int32_t*)W(w_kk), (int32_t*)W(w_kd),
+                (int32_t*)W(w_kn), (int32_t*)W(w_kg), (double*)W(w_kp), (double*)W(w_ks),
+                (int32_t*)W(w_pb), (int32_t*)W(w_pn), (int64_t*)W(w_ca), (int32_t*)W(w_cnt)};
+  plan_emit_kernel<<<1, kEmitThreads, 0, ctx->stream>>>(pd.ds, pd.rec, a, o);
+  PSG_CUDA(cudaGetLastError());
+  // one D2H of the emitted region (sized for every candidate), then trim
+  PSG_CUDA(ctx->h_out.ensure(ok.size + 64));
+  PSG_CUDA(cudaMemcpyAsync(ctx->h_out.p, w, ok.size, cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const unsigned char* h = static_cast<const unsigned char*>(ctx->h_out.p);
+  auto Hi = [&](size_t off) { return reinterpret_cast<const int32_t*>(h + off); };
+  auto Hd = [&](size_t off) { return reinterpret_cast<const double*>(h + off); };
+  const int np = Hi(w_cnt)[0], nk = Hi(w_cnt)[1], nb = Hi(w_cnt)[2];
+  if (np == 0) return fail(ctx, PSG_ERR_INFEASIBLE, "no parallel execution plan fits the model on this cluster");
+  auto* so = new PlanSoaOwned();
+  auto take_i = [&](std::vector<int32_t>& v, size_t off, size_t n) { v.assign(Hi(off), Hi(off) + n); };
+  auto take_d = [&](std::vector<double>& v, size_t off, size_t n) { v.assign(Hd(off), Hd(off) + n); };
+  take_i(so->dp, w_dp, np); take_i(so->st, w_st, np); take_i(so->sd, w_sd, np);
+  take_i(so->reps, w_rp, np); take_i(so->dt, w_dt, np); take_i(so->enc, w_en, np);
+  take_d(so->kv, w_kv, np); take_d(so->bud, w_bu, np); take_d(so->ppt, w_pp, np);
+  take_d(so->hid, w_hi, np); take_d(so->head, w_he, np); take_d(so->kve, w_ke, np);
+  take_i(so->cb, w_cb, size_t(np) + 1); take_i(so->cop, w_co, size_t(np) * nc);
+  take_d(so->ct, w_ct, size_t(np) * nc); take_d(so->cw, w_cw, size_t(np) * nc);
+  take_d(so->cs, w_cs, size_t(np) * nc); take_i(so->kb, w_kb, size_t(np) + 1);
+  take_i(so->kk, w_kk, nk); take_i(so->kd, w_kd, nk); take_i(so->kn, w_kn, nk); take_i(so->kg, w_kg, nk);
+  take_d(so->kp, w_kp, nk); take_d(so->ksh, w_ks, nk);
+  take_i(so->pb, w_pb, size_t(np) + 1); take_i(so->pn, w_pn, nb);
+  so->cand.assign(reinterpret_cast<const int64_t*>(h + w_ca), reinterpret_cast<const int64_t*>(h + w_ca) + np);
+  auto nz = [](auto& v) { return v.empty() ? nullptr : v.data(); };
+  psg_plan_set& v = so->set;
+  v = psg_plan_set{np, nz(so->dp), nz(so->st), nz(so->sd), nz(so->reps), nz(so->dt), nz(so->enc),
+                   nz(so->kv), nz(so->bud), nz(so->ppt), nz(so->hid), nz(so->head), nz(so->kve),
+                   so->cb.data(), nz(so->cop), nz(so->ct), nz(so->cw), nz(so->cs), so->kb.data(),
+                   nz(so->kk), nz(so->kd), nz(so->kn), nz(so->kg), nz(so->kp), nz(so->ksh),
+                   so->pb.data(), nz(so->pn)};
+  so->candidate = so->cand.data();
+  *out = so;
+  return PSG_OK;
+}
+
+int plan_emit(psg_context* ctx, const psg_plan_space* s, const psg_plan_emit_in* in, psg_plan_soa** out) {
+  return guarded(ctx, [&] { return plan_emit_impl(ctx, s, in, out); });
+}
+
+void plan_soa_free(psg_plan_soa* soa) { delete static_cast<PlanSoaOwned*>(soa); }
 
 }  // namespace psg
 

@@ -15,6 +15,10 @@
 //                          (planner.cpp:121-152) resolved against the group's
 //                          spans, and the memory ledger (finalize_plan,
 //                          planner.cpp:307-370) in the reference's order.
+//   plan_emit_kernel       the kept candidates compacted into the psg_plan_set
+//                          SoA the search consumes (psg_plan_emit).
+#include <cub/block/block_scan.cuh>
+
 #include "psg_device.cuh"
 #include "psg_reduce.cuh"
 
@@ -194,6 +198,102 @@ __global__ void __launch_bounds__(128) plan_candidate_kernel(const psg_plan_spac
   out[idx] = r;
 }
 
+// plan_emit_kernel: one block compacts the kept candidates (host keep flag
+// = first occurrence of the encoding, device feasibility) in candidate order
+// straight into the psg_plan_set arrays (PlanSoA's layout, search.cpp), three
+// block scans per 1024-candidate tile: plan index, collective offset, p2p
+// offset.
+__global__ void __launch_bounds__(kEmitThreads) plan_emit_kernel(const psg_plan_space s,
+                                                                 const psg_plan_record* rec,
+                                                                 const PlanEmitArgs a,
+                                                                 PlanEmitOut o) {
+  using Scan = cub::BlockScan<int, kEmitThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry[3];
+  const int64_t total = s.group_first[s.n_groups];
+  const int nc = s.n_cells;
+  if (threadIdx.x == 0) carry[0] = carry[1] = carry[2] = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < total; t0 += kEmitThreads) {
+    const int64_t idx = t0 + threadIdx.x;
+    int g = 0;
+    bool kept = false;
+    if (idx < total) {
+      int lo = 0, hi = s.n_groups - 1;  // group of this candidate
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        if (s.group_first[mid] <= idx) lo = mid; else hi = mid - 1;
+      }
+      g = lo;
+      kept = a.keep[idx] && rec[idx].feasible;
+    }
+    const int nk = kept ? rec[idx].n_colls : 0, np2 = kept ? s.group_stages[g] - 1 : 0;
+    int pi, ko, po, tp, tk, tpp;
+    Scan(tmp).ExclusiveSum(int(kept), pi, tp);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(nk, ko, tk);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(np2, po, tpp);
+    pi += carry[0];
+    ko += carry[1];
+    po += carry[2];
+    if (kept) {
+      const psg_plan_record& r = rec[idx];
+      o.model_dp[pi] = s.group_dp[g];
+      o.num_stages[pi] = s.group_stages[g];
+      o.stage_devices[pi] = s.group_sdev[g];
+      o.stage_reps[pi] = s.group_reps[g];
+      o.dtype[pi] = a.compute_dtype;
+      o.enc_rank[pi] = a.enc_rank[idx];
+      o.kv[pi] = r.kv_bytes_per_token;
+      o.budget[pi] = r.kv_budget_per_replica;
+      o.p2p_ppt[pi] = a.payload_per_token;
+      o.sh_hidden[pi] = a.shape_hidden;
+      o.sh_head[pi] = a.shape_head_dim;
+      o.sh_kv[pi] = a.shape_kv_elems;
+      o.candidate[pi] = idx;
+      int64_t k = idx - s.group_first[g];
+      for (int ci = nc - 1; ci >= 0; --ci) {  // mixed radix, last cell fastest
+        const int b = s.choice_begin[g * nc + ci], m = s.choice_begin[g * nc + ci + 1] - b;
+        const int c = b + int(k % m);
+        k /= m;
+        const int q = pi * nc + ci;
+        o.cell_op[q] = a.ch_op[c];
+        o.cell_tasks[q] = a.ch_tasks[c];
+        o.cell_width[q] = a.ch_width[c];
+        o.cell_scale[q] = a.ch_scale[c];
+      }
+      o.cell_begin[pi] = pi * nc;
+      o.coll_begin[pi] = ko;
+      for (int q = 0; q < r.n_colls; ++q) {
+        o.coll_kind[ko + q] = r.coll_kind[q];
+        o.coll_devices[ko + q] = r.coll_devices[q];
+        o.coll_nodes[ko + q] = r.coll_nodes[q];
+        o.coll_groups[ko + q] = r.coll_groups[q];
+        o.coll_ppt[ko + q] = a.payload_per_token;
+        o.coll_share[ko + q] = r.coll_share[q];
+      }
+      o.p2p_begin[pi] = po;
+      for (int b = 0; b < np2; ++b) o.p2p_nodes[po + b] = a.p2p[a.p2p_off[g] + b];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry[0] += tp;
+      carry[1] += tk;
+      carry[2] += tpp;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // the closing offsets and the counts
+    o.cell_begin[carry[0]] = carry[0] * nc;
+    o.coll_begin[carry[0]] = carry[1];
+    o.p2p_begin[carry[0]] = carry[2];
+    o.counts[0] = carry[0];
+    o.counts[1] = carry[1];
+    o.counts[2] = carry[2];
+  }
+}
+
 }  // namespace psg
 
 extern "C" int psg_plan_compute(psg_context* ctx, const psg_plan_space* space,
@@ -201,3 +301,10 @@ extern "C" int psg_plan_compute(psg_context* ctx, const psg_plan_space* space,
                                 int32_t* p2p) {
   return psg::plan_compute(ctx, space, records, phys, p2p_offset, p2p);
 }
+
+extern "C" int psg_plan_emit(psg_context* ctx, const psg_plan_space* space, const psg_plan_emit_in* in,
+                             psg_plan_soa** out) {
+  return psg::plan_emit(ctx, space, in, out);
+}
+
+extern "C" void psg_plan_soa_free(psg_plan_soa* soa) { psg::plan_soa_free(soa); }

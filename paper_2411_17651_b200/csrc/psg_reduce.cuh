@@ -47,6 +47,36 @@ __global__ void plan_map_kernel(const psg_plan_space s, int32_t* phys_out, const
                                 int32_t* p2p_out, int32_t* span_nodes, int32_t* span_level);
 __global__ void plan_candidate_kernel(const psg_plan_space s, const int32_t* span_nodes,
                                       psg_plan_record* out);
+// plan_emit_kernel arguments: host per-candidate / per-choice values (device
+// copies) and the psg_plan_set arrays it fills (device, sized for every
+// candidate kept); counts = {plans, collectives, p2p boundaries}.
+struct PlanEmitArgs {
+  const uint8_t* keep;
+  const int32_t* enc_rank;
+  const int32_t* ch_op;
+  const double *ch_tasks, *ch_width, *ch_scale;
+  const int64_t* p2p_off;  // [groups + 1] into p2p (group boundary node counts)
+  const int32_t* p2p;
+  int32_t compute_dtype;
+  double payload_per_token, shape_hidden, shape_head_dim, shape_kv_elems;
+};
+struct PlanEmitOut {
+  int32_t *model_dp, *num_stages, *stage_devices, *stage_reps, *dtype, *enc_rank;
+  double *kv, *budget, *p2p_ppt, *sh_hidden, *sh_head, *sh_kv;
+  int32_t *cell_begin, *cell_op;
+  double *cell_tasks, *cell_width, *cell_scale;
+  int32_t *coll_begin, *coll_kind, *coll_devices, *coll_nodes, *coll_groups;
+  double *coll_ppt, *coll_share;
+  int32_t *p2p_begin, *p2p_nodes;
+  int64_t* candidate;
+  int32_t* counts;
+};
+constexpr int kEmitThreads = 1024;
+__global__ void plan_emit_kernel(const psg_plan_space s, const psg_plan_record* rec,
+                                 const PlanEmitArgs a, PlanEmitOut o);
+int plan_emit(psg_context* ctx, const psg_plan_space* s, const psg_plan_emit_in* in,
+              psg_plan_soa** out);
+void plan_soa_free(psg_plan_soa* soa);
 int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* records,
                  int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
 __global__ void sim_kernel(const SimParams p);       // one warp per block

@@ -40,6 +40,7 @@ def _lib():
     lib.psgh_trace_load.argtypes = [v, C.c_char_p]
     lib.psgh_plans_generate.argtypes = [v]
     lib.psgh_plans_generate_device.argtypes = [v]
+    lib.psgh_plans_generate_direct.argtypes = [v]
     lib.psgh_plan_build.argtypes = [v, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     lib.psgh_plans_count.argtypes = [v]
@@ -120,8 +121,11 @@ class Problem:
 
     def generate_plans(self, device=False):
         """generate_plans (planner.cpp:375-389); device=True maps and finalizes
-        the candidates on the GPU (the same plans, field for field)."""
-        fn = self.lib.psgh_plans_generate_device if device else self.lib.psgh_plans_generate
+        the candidates on the GPU (the same plans, field for field);
+        device="direct" also compacts them on the GPU straight into the plan
+        SoA the search consumes (no ExecutionPlans on the host)."""
+        fn = (self.lib.psgh_plans_generate_direct if device == "direct" else
+              self.lib.psgh_plans_generate_device if device else self.lib.psgh_plans_generate)
         self._check(fn(self.h))
         return self
 
@@ -161,6 +165,8 @@ class Problem:
     # ---- dumps (parity tests) ----
     def _string(self, fn):
         p = fn(self.h)
+        if not p:
+            raise from_code(abi.PSG_ERR_USAGE, self.lib.psgh_last_error().decode())
         try:
             return C.string_at(p).decode()
         finally:
