@@ -19,7 +19,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxCells = 8;      // cells per block (the reference IR emits 2)
 constexpr int kMaxClampSlots = 64;  // collectives + distinct p2p curves of a plan
 constexpr int kWindow = 32;         // prefetched upcoming requests per unit
-constexpr int kProfSlots = 26;      // phase-profile counters per unit (dev builds)
+constexpr int kProfSlots = 32;      // phase-profile counters per unit (dev builds)
 
 // ---------------------------------------------------------------------------
 // Device views of the ABI inputs (all pointers are device pointers).

@@ -54,7 +54,10 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 // 16 cycles waited for speculation results, 17 eval cycles of misses,
 // speculation misses by cause: 18 no job, 19 not one item, 20 other decode
 // count, 21 other tokens, 22 job not started; own evaluations: 23 query
-// values (loads + curves), 24 the four chains, 25 stage pass.
+// values (loads + curves), 24 the four chains, 25 stage pass; slot-array
+// mode: 26 finish cycles, 27 #finish events, 28 #admissions, 29 #mixed,
+// 30 cycles of admit passes that admitted, 31 cycles of outer passes that
+// started in slot-array mode.
 #ifdef PSG_PHASE_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(slot, v) (prof_acc[slot] += (unsigned long long)(clock64() - (v)))
@@ -64,6 +67,12 @@ constexpr int kGF64 = 4;  // adm, ft, arr, fin
 #define PROF_ADD(slot, v)
 #define PROF_CNT(slot)
 #endif
+
+// Warp sum of 32-bit lane values without 32-bit overflow (two REDUX).
+__device__ __forceinline__ int64_t warp_sum_wide(unsigned v) {
+  return int64_t(__reduce_add_sync(kFull, v & 0xffffu)) +
+         (int64_t(__reduce_add_sync(kFull, v >> 16)) << 16);
+}
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
   return (a < b) ? b : a;  // std::max(a, b)
@@ -90,8 +99,9 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 //   PSG_PIPE_MIN  shortest decode run stepped by the software-pipelined loop
 //   PSG_FILL_B    live slots at or below which a finish returns the batch to
 //                 lane-resident slots
-//   PSG_DIRECT_CHUNKS  slot-array finishes of at most this many 32-slot chunks
-//                 finish every chunk at once instead of walking the summary
+//   PSG_SHORT_COLS  short slot-array mode: while at most 32 x this many slots
+//                 are in use, lane l mirrors the finish iteration of slots
+//                 l, 32+l, ... in registers and the finish summary is not kept
 #ifndef PSG_REG_ALL
 #define PSG_REG_ALL 0
 #endif
@@ -101,8 +111,8 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~size_t(
 #ifndef PSG_FILL_B
 #define PSG_FILL_B 32
 #endif
-#ifndef PSG_DIRECT_CHUNKS  // slot-array finishes: batches of <= 32x this many slots skip the summary walk
-#define PSG_DIRECT_CHUNKS 4
+#ifndef PSG_SHORT_COLS  // slot-array batches of <= 32x this many slots keep their finish iterations in registers
+#define PSG_SHORT_COLS 4
 #endif
 constexpr int kMemoCap = 256;  // decode-cost memo entries (SimParams::memo_cap must match)
 
@@ -563,6 +573,16 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   // fill() switches back once the batch is small again.
   constexpr bool kReg = kSpec || PSG_REG_ALL;
   bool regm = kReg;
+  // Short slot-array mode (!regm, len <= kShortCap): a.fin stays the source
+  // of truth, lane l mirrors positions l, 32+l, ... in sf[] so a finish is a
+  // register compare + ballot instead of a summary walk; cm1 / cm2 are not
+  // maintained (rebuilt on leaving the mode).
+  constexpr int kSC = PSG_SHORT_COLS > 0 ? PSG_SHORT_COLS : 1;
+  constexpr int kShortCap = PSG_SHORT_COLS > 0 ? kSC * kWarp : 0;
+  bool shm = !kReg && kShortCap > 0;
+  int64_t sf[kSC];
+#pragma unroll
+  for (int h = 0; h < kSC; ++h) sf[h] = kDead;
   int32_t r_tidx = 0, r_ctx = 0, r_gen = 0, r_done = 0, r_slot = 0;
   int64_t r_fin = kDead;
   double r_adm = 0.0, r_ft = 0.0, r_arr = 0.0;
@@ -653,6 +673,17 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     for (int c = 0; c < nch; ++c) fix_chunk(c);
     for (int g = 0; g * kWarp < nch; ++g) fix_group(g);
   };
+  // short slot-array mode: mirror a.fin of positions < len into sf[]
+  auto sf_load = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < kSC; ++h) sf[h] = h * kWarp + lane < len ? a.fin[h * kWarp + lane] : kDead;
+  };
+  auto sf_set = [&](int pos, int64_t v) {  // the owner lane of position pos
+#pragma unroll
+    for (int h = 0; h < kSC; ++h)
+      if (h * kWarp + lane == pos) sf[h] = v;
+  };
   // Order-preserving in-place compaction of the live slots.
   auto compact = [&]() {
     __syncwarp();
@@ -693,7 +724,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
     len = w;
     first_pre = below;
-    rebuild_summary();
+    if (shm) sf_load(); else rebuild_summary();
   };
   auto migrate = [&]() {
     // Move the (compacted) active slots to the unit's global region: capacity n_req.
@@ -743,6 +774,13 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     first_pre = first_pre < len ? first_pre : len;
   };
   auto recompute_next_fin = [&]() {
+    if (shm) {
+      unsigned m = kNoRel;
+#pragma unroll
+      for (int h = 0; h < kSC; ++h) m = min(m, min_rel(sf[h], n));
+      next_fin = abs_of(__reduce_min_sync(kFull, m));
+      return;
+    }
     const int ng = ((len + kWarp - 1) / kWarp + kWarp - 1) / kWarp;
     unsigned m = kNoRel;
     for (int base = 0; base < ng; base += kWarp) {
@@ -766,7 +804,15 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
     const unsigned pm = __ballot_sync(kFull, lane < len && r_fin == kNoFin);
     first_pre = pm ? __ffs(pm) - 1 : len;
-    rebuild_summary();
+    if (kShortCap > 0) {  // into the short slot-array mode
+      sf[0] = lane < len ? r_fin : kDead;
+#pragma unroll
+      for (int h = 1; h < kSC; ++h) sf[h] = kDead;
+      shm = true;
+      __syncwarp();
+    } else {
+      rebuild_summary();
+    }
     regm = false;
   };
   // slot arrays -> lane-resident slots (len <= kWarp)
@@ -786,6 +832,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
     __syncwarp();
     regm = kReg;
+    shm = false;
   };
   // order-preserving compaction of the lane-resident slots (staged through
   // the otherwise unused slot arrays)
@@ -816,7 +863,20 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   // call site of load_head for a smaller loop body)
   bool head_dirty = kReg;
   if (!kReg) load_head();
+#ifdef PSG_PHASE_PROFILE
+  long long pass_t = clock64();
+  bool pass_arr = false;
+#endif
   while (true) {
+#ifdef PSG_PHASE_PROFILE
+    {
+      const long long now = clock64();
+      if (pass_arr) prof_acc[31] += (unsigned long long)(now - pass_t);
+      pass_t = now;
+      pass_arr = !regm;
+    }
+    const int64_t adm0 = admissions;
+#endif
     // ---- admit (batching.cpp:35-60) ----
     PROF_T0(t_adm);
     while (true) {
@@ -845,13 +905,23 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
             r_arr = hd_arr;
           }
         } else {
+          if (shm && len == kShortCap) {  // the short mode is full
+            if (B < len) compact();
+            if (len == kShortCap) {
+              rebuild_summary();
+              shm = false;
+            }
+          }
           if (len >= cap_now) {
             if (len > B) compact();
             if (len >= cap_now) migrate();
           }
+          if (shm) sf_set(len, kNoFin);
           if (lane == 0) {
-            if ((len & (kWarp - 1)) == 0) cm1[len / kWarp] = kNoFin;  // fresh chunk / group
-            if ((len & (kWarp * kWarp - 1)) == 0) cm2[len / (kWarp * kWarp)] = kNoFin;
+            if (!shm) {
+              if ((len & (kWarp - 1)) == 0) cm1[len / kWarp] = kNoFin;  // fresh chunk / group
+              if ((len & (kWarp * kWarp - 1)) == 0) cm2[len / (kWarp * kWarp)] = kNoFin;
+            }
             a.tidx[len] = hd_tidx;
             a.ctx[len] = hd_ctx;
             a.gen[len] = hd_gen;
@@ -876,6 +946,12 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     }
     __syncwarp();
     PROF_ADD(0, t_adm);
+#ifdef PSG_PHASE_PROFILE
+    if (admissions != adm0) {
+      prof_acc[30] += (unsigned long long)(clock64() - t_adm);
+      if (!regm) prof_acc[28] += (unsigned long long)(admissions - adm0);
+    }
+#endif
 
     if (B == 0) {  // idle (simulator.cpp:116-120)
       if (!hd_valid) break;
@@ -890,6 +966,9 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       // ---- mixed iteration (batching.cpp:62-108): prefill items from the
       // prefill frontier, decode count = the rest ----
       PROF_CNT(10);
+#ifdef PSG_PHASE_PROFILE
+      if (!regm) prof_acc[29] += 1ull;
+#endif
       PROF_T0(t_m1);
       int n_items = 0;
       int64_t pre_tok = 0;
@@ -1044,6 +1123,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         const int i = base + lane;
         bool compl_now = false, still = false;
         unsigned rel = kNoRel;
+        int64_t fin = kDead;
         if (i < len && a.fin[i] == kNoFin) {
           const int32_t ctx = a.ctx[i];
           int64_t tok = int64_t(ctx) - a.done[i];
@@ -1052,7 +1132,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
           a.done[i] = int32_t(done);
           if (done == ctx) {  // the prefill iteration samples the first token
             const int32_t gen = a.gen[i];
-            const int64_t fin = n_new + (gen > 1 ? gen - 1 : 0);
+            fin = n_new + (gen > 1 ? gen - 1 : 0);
             a.fin[i] = fin;
             a.ft[i] = clock;
             compl_now = true;
@@ -1061,10 +1141,16 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
             still = true;
           }
         }
+        if (shm) {  // mirror the new decode slots
+          const int c = base / kWarp;
+#pragma unroll
+          for (int h = 0; h < kSC; ++h)
+            if (compl_now && h == c) sf[h] = fin;
+        }
         ncompl += __popc(__ballot_sync(kFull, compl_now));
         const unsigned cr = __reduce_min_sync(kFull, rel);
         m = min(m, cr);
-        if (cr != kNoRel && lane == 0) {  // new decode slots in this chunk
+        if (!shm && cr != kNoRel && lane == 0) {  // new decode slots in this chunk
           const int64_t v = n_new + int64_t(cr);
           const int c = base / kWarp;
           cm1[c] = min(cm1[c], v);
@@ -1278,6 +1364,9 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     // (simulator.cpp:143-156) at iteration n; finished slots become
     // tombstones ----
     PROF_T0(t_fin);
+#ifdef PSG_PHASE_PROFILE
+    const bool regm_fin = regm || next_fin != n;
+#endif
     if (next_fin == n) {  // finishes at this iteration
       if (regm) {
         PROF_CNT(13);
@@ -1301,6 +1390,53 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         used -= freed;
         next_fin = abs_of(m);
         reg_trim();
+      } else if (shm) {
+        // short slot-array mode: this lane's finishing positions as a bit
+        // set (positions >= len mirror kDead, which never equals n)
+        PROF_CNT(13);
+        unsigned fb = 0, lm = kNoRel;
+#pragma unroll
+        for (int h = 0; h < kSC; ++h) {
+          const bool f = sf[h] == n;
+          fb |= unsigned(f) << h;
+          lm = min(lm, f ? kNoRel : min_rel(sf[h], n));
+          sf[h] = f ? kDead : sf[h];
+        }
+        unsigned tok = 0, nf = 0;  // <= kSC slots of < 2^27 tokens per lane (< 2^32)
+        while (__any_sync(kFull, fb != 0)) {  // usually one pass: one finish per lane
+          if (fb) {
+            const int i = (__ffs(fb) - 1) * kWarp + lane;
+            fb &= fb - 1;
+            const int32_t gen = a.gen[i];
+            const double arr = a.arr[i], ft = a.ft[i];
+            const double anchor = p.anchor == PSG_ANCHOR_ARRIVAL ? arr : a.adm[i];
+            const size_t s = slot_base + a.slot[i];
+            p.slot_e2e[s] = __dsub_rn(clock, arr);
+            p.slot_ttft[s] = __dsub_rn(ft, anchor);
+            p.slot_tpot[s] = __dsub_rn(clock, ft);  // / (gen - 1) in entry_reduce_kernel
+            p.slot_status[s] = 1;
+            a.fin[i] = kDead;
+            tok += unsigned(a.ctx[i] + (gen > 1 ? gen : 1));  // the ledger holds ctx + max(gen, 1)
+            ++nf;
+          }
+        }
+        const int64_t freed = warp_sum_wide(tok);
+        const int nfin = int(__reduce_add_sync(kFull, nf));
+        B -= nfin;
+        completed += nfin;
+        used -= freed;
+        next_fin = abs_of(__reduce_min_sync(kFull, lm));
+        int nl = 0;  // trim: 1 + the newest live position
+#pragma unroll
+        for (int h = kSC - 1; h >= 0; --h) {
+          const unsigned lv = __ballot_sync(kFull, sf[h] != kDead);
+          if (nl == 0 && lv) nl = h * kWarp + kWarp - __clz(lv);
+        }
+        len = nl;
+        first_pre = first_pre < len ? first_pre : len;
+        const bool small = kReg && B <= PSG_FILL_B;  // small again: back to lane-resident slots
+        if (small && len > B) compact();
+        if (small) fill();
       } else {
         PROF_CNT(13);
         int64_t freed = 0;
@@ -1364,10 +1500,21 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         trim();
         const bool small = kReg && B <= PSG_FILL_B;  // small again: back to lane-resident slots
         if (len > 2 * B + 2 * kWarp || (small && len > B)) compact();
-        if (small) fill();
+        if (small) {
+          fill();
+        } else if (len <= kShortCap && cap_now == p.smem_cap) {  // into the short mode
+          sf_load();
+          shm = true;
+        }
       }
     }
     PROF_ADD(7, t_fin);
+#ifdef PSG_PHASE_PROFILE
+    if (!regm_fin) {
+      prof_acc[26] += (unsigned long long)(clock64() - t_fin);
+      prof_acc[27] += 1ull;
+    }
+#endif
     // ---- LIFO eviction on overflow (batching.cpp:110-125) ----
     PROF_T0(t_evi);
     if (used > cap_tok) {  // KV overflow (rare): the block below
@@ -1397,11 +1544,12 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
           g_stack[stack_top] = a.tidx[i];  // push_front of pending
           a.fin[i] = kDead;
         }
+        if (shm) sf_set(i, kDead);
         ++stack_top;
         --B;
         evicted = true;
         trim();
-        if (fin != kNoFin) {  // a decode slot left the summary
+        if (!shm && fin != kNoFin) {  // a decode slot left the summary
           fix_chunk(i / kWarp);
           fix_group(i / (kWarp * kWarp));
         }
@@ -1412,6 +1560,9 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         used = 0;
         next_fin = kNoFin;
         regm = kReg;  // empty: lane-resident
+        shm = !kReg && kShortCap > 0;
+#pragma unroll
+        for (int h = 0; h < kSC; ++h) sf[h] = kDead;
       }
       __syncwarp();
       if (evicted) {  // the evicted requests wait at the queue head (batching.cpp:114-118)

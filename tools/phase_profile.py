@@ -20,13 +20,16 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 NAMES = ["admit", "mixed_scan", "mixed_eval", "mixed_adv", "dec_cost", "run_setup", "tight",
          "finish", "evict", "refill", "#mixed", "#runs", "#dec_eval", "#finish", "#spec_hits", "total",
          "spec_wait_cyc", "miss_eval_cyc", "miss_nojob", "miss_items", "miss_decode", "miss_tok",
-         "miss_unstarted", "ev_query_cyc", "ev_chain_cyc", "ev_stage_cyc"]
+         "miss_unstarted", "ev_query_cyc", "ev_chain_cyc", "ev_stage_cyc",
+         "arr_finish_cyc", "#arr_finish", "#arr_admit", "#arr_mixed", "admit_adm_cyc", "arr_pass_cyc"]
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("keys", nargs="+")
     ap.add_argument("--top", type=int, default=5)
+    ap.add_argument("--enc", action="append", default=[], help="also show units whose encoding contains this")
+    ap.add_argument("--per-dp", action="store_true", help="the longest unit of each DP degree instead of the top units")
     ap.add_argument("--workdir", default="/tmp/psg_probe")
     ap.add_argument("--native", action="store_true",
                     help="build inputs with the native host library instead of the reference driver")
@@ -78,7 +81,23 @@ def run(key, args):
     print(f"{args.key}: sim {res.ms['sim']:.2f} ms, units {len(raw)}, "
           f"sum/max {tots.sum() / tots.max():.1f}, units >50% of max: {(tots > 0.5 * tots.max()).sum()}, "
           f"totals: {' '.join(f'{k}={cnt[:, k].sum()}' for k in range(10, 14))}")
-    for u in order[:args.top]:
+    by_dp = {}
+    for u in range(len(cnt)):
+        enc = case.plans.encodings[int(meta[u, 0]) // F]
+        by_dp.setdefault(enc.split(":")[0], []).append(float(cnt[u, 15]) / 1.965e6)
+    print("  by DP: " + "  ".join(f"{k}: n={len(v)} max={max(v):.2f} med={sorted(v)[len(v) // 2]:.2f} ms"
+                                  for k, v in sorted(by_dp.items(), key=lambda kv: -max(kv[1]))))
+    shown = order[:args.top]
+    if args.per_dp:
+        seen, shown = set(), []
+        for u in order:
+            dp = case.plans.encodings[int(meta[u, 0]) // F].split(":")[0]
+            if dp not in seen:
+                seen.add(dp)
+                shown.append(u)
+    shown = list(shown) + [u for u in order if u not in set(shown) and any(
+        e in case.plans.encodings[int(meta[u, 0]) // F] for e in args.enc)]
+    for u in shown:
         tot = float(cnt[u, 15])
         enc = case.plans.encodings[int(meta[u, 0]) // F]
         parts = " ".join(f"{NAMES[k]}={100 * cnt[u, k] / tot:.1f}%" for k in range(10))
@@ -88,6 +107,11 @@ def run(key, args):
         counts += " | " + " ".join(f"{NAMES[k]}={int(cnt[u, k])}" for k in range(18, 23))
         own = max(1, int(cnt[u, 10]) - int(cnt[u, 14]))
         counts += " | per own eval: " + " ".join(f"{NAMES[k]}={int(cnt[u, k]) // own}" for k in range(23, 26))
+        if cnt.shape[1] > 26 + 5:
+            counts += (f" | slot-array mode: {100 * cnt[u, 31] / tot:.1f}% of cycles, finish "
+                       f"{int(cnt[u, 26]) // max(1, int(cnt[u, 27]))} cyc x {int(cnt[u, 27])}, "
+                       f"admissions {int(cnt[u, 28])}, mixed {int(cnt[u, 29])}; admitting passes "
+                       f"{100 * cnt[u, 30] / tot:.1f}% of cycles")
         print(f"  {enc} r{int(meta[u, 1])}: {tot / 1.965e6:.2f} ms @1965MHz | {parts} | {counts}")
 
 
