@@ -64,14 +64,17 @@ struct Unit {
   int64_t scratch;     // offset (elements) into the per-unit global scratch
   int64_t gtab;        // staged curves in SimParams::g_tab at this offset (doubles), or -1:
                        // shared memory (they fit the launch's per-unit budget)
+  int64_t log_off;     // chain_replicas == 2, replica >= 1: tally log at SimParams::rlog + log_off
+  int32_t log_cap;     // ... holding at most this many records
+  int32_t pad;
 };
 
 struct UnitOut {
   double clock, energy, flops, bytes;
   int64_t iterations, max_batch, completed, rejected;
   int64_t sum_batch, admissions;  // work counters (algorithmic bytes)
-  int32_t err;         // 0 ok, 1 chunk_size < 1, 2 missing table
-  int32_t pad;
+  int32_t err;         // 0 ok, 1 chunk_size < 1, 2 missing table, 9 tally log overflow (internal)
+  int32_t nlog;        // tally records logged (chain_replicas == 2, replica >= 1)
 };
 
 struct SimParams {
@@ -95,7 +98,11 @@ struct SimParams {
   int32_t smem_cap;          // active-list capacity held in shared memory
   int32_t memo_cap;          // decode-cost memo entries in shared memory
   int32_t serial_run;        // decode runs longer than this take the closed form
-  int32_t chain_replicas;    // 1: grid = entries, replicas run in order with one tally
+  int32_t chain_replicas;    // 1: grid = entries, replicas run in order with one tally;
+                             // 2: grid = replica groups (block_k0/k1), each group's replicas
+                             // in order on one warp, groups concurrently, the last group to
+                             // finish replays the tally from the later groups' logs;
+                             // 0: grid = units, per-replica tallies (dev)
   int32_t speculate;         // 1: blockDim 64, a second warp prices the next mixed iteration
   int32_t spec_sleep_ns;     // the speculation warp's polling interval
   const int32_t* entry_unit_begin;  // [E+1] units of entry e (replica order) ...
@@ -129,6 +136,11 @@ struct SimParams {
   int32_t* g_i32;            // kGI32 int32 arrays per unit, stride n_req
   double* g_f64;             // kGF64 8-byte arrays per unit, stride n_req
   int64_t* g_cm;             // per-unit chunk minima once the active slots live in global memory
+  double2* rlog;             // chain_replicas == 2: tally logs (Unit::log_off)
+  int32_t* entry_done;       // chain_replicas == 2: groups finished per entry (zeroed per launch)
+  const int32_t* block_k0;   // chain_replicas == 2: block b runs entry_units[block_k0[b] .. block_k1[b])
+  const int32_t* block_k1;
+  const int32_t* entry_groups;  // chain_replicas == 2: groups of entry e
 };
 
 // Parameters of the cost-table kernels (psg_tables.cu).

@@ -146,13 +146,15 @@ struct psg_context {
   int n_sm = 148;                  // device properties used to size the simulation launch
   int64_t smem_sm = 228 * 1024, smem_block_max = 227 * 1024;
   int concurrent_blocks = 0;       // psg_search_many: simulation blocks sharing the device
+  int concurrent_groups = 0;       // ... as replica-group blocks (SimParams::chain_replicas 2)
+  bool chain_fallback = false;     // rerun with chained replicas (a tally log overflowed)
   int64_t sim_static_smem = 0;     // sim_kernel's static shared memory
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
   DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
   HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
-  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan, d_gtab;
+  DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan, d_gtab, d_rlog, d_edone;
   // storage for results handed out (valid until the next call)
   std::vector<psg_entry> entries;
   std::vector<uint8_t> compute_clamp, curve_clamp;
@@ -160,8 +162,18 @@ struct psg_context {
 
 namespace {
 
+// Replica groups per DP>1 entry (SimParams::chain_replicas 2).
+int replica_groups() {
+  if (const char* v = std::getenv("PSG_REPLICA_GROUPS")) return std::max(1, std::atoi(v));  // dev knob
+  return 2;
+}
+
 void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
   const bool chunked = sp.batch_mode == PSG_BATCH_CHUNKED;
+  if (const char* v = std::getenv("PSG_CARVEOUT"))  // dev knob: shared-memory carve-out, percent
+    for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+                          (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked})
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(v));
   if (sp.emit_it)
     sim_kernel_emit<<<blocks, kWarp, smem, st>>>(sp);
   else if (sp.speculate)
@@ -527,7 +539,8 @@ void psg_context_destroy(psg_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
                     &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
-                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan, &ctx->d_gtab})
+                    &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan, &ctx->d_gtab,
+                    &ctx->d_rlog, &ctx->d_edone})
     b->release();
   for (HostBuf* b : {&ctx->h_in, &ctx->h_out, &ctx->h_pr, &ctx->h_rj, &ctx->h_it, &ctx->h_isec, &ctx->h_ijou})
     b->release();
@@ -777,6 +790,9 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       off += u.n_req;
       u.scratch = 0;
       u.gtab = -1;
+      u.log_off = -1;
+      u.log_cap = 0;
+      u.pad = 0;
       units.push_back(u);
     }
   }
@@ -806,6 +822,60 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   int64_t scratch_total = 0;
   for (const auto& u : units) scratch_total += u.n_req;
   const int n_units = int(units.size());
+
+  // ---- replica mode (SimParams::chain_replicas) ----
+  // 2 (default): an entry's DP replicas split into up to `groups` contiguous
+  // groups; a group's replicas run in order on one warp carrying the tally,
+  // groups run concurrently, and the entry's last group to finish replays
+  // the WorkTally from the later groups' logs (the longest DP>1 entries then
+  // stop bounding the search); 1: one group per entry (iteration-record
+  // pass, and the fallback when a log overflows); 0: one warp per replica
+  // with per-replica tallies (dev).
+  int chain = (cfg->emit_iterations || ctx->chain_fallback) ? 1 : 2;
+  if (const char* v = std::getenv("PSG_CHAIN_REPLICAS"))  // dev knob
+    if (!ctx->chain_fallback) chain = std::max(0, std::min(2, std::atoi(v)));
+  const int groups = replica_groups();
+  int64_t rlog_total = 0;
+  std::vector<int32_t> block_k0, block_k1, entry_groups(E, 1);
+  if (chain == 2) {
+    struct Blk { int32_t k0, k1; int64_t work; };
+    std::vector<Blk> blks;
+    for (int e = 0; e < E; ++e) {
+      const int k0 = entry_unit_begin[e], R = entry_unit_begin[e + 1] - k0;
+      const int G = std::max(1, std::min(R, groups));
+      entry_groups[e] = G;
+      for (int g = 0; g < G; ++g) {
+        const int a = k0 + int(int64_t(g) * R / G), b = k0 + int(int64_t(g + 1) * R / G);
+        int64_t w = 0;
+        for (int k = a; k < b; ++k) w += units[entry_units[k]].n_req;
+        blks.push_back({a, b, w});
+      }
+    }
+    std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.work > y.work; });
+    for (const Blk& b : blks) {
+      block_k0.push_back(b.k0);
+      block_k1.push_back(b.k1);
+    }
+    // records: one per mixed iteration or decode run; a request causes at
+    // most ~4 of them plus its prefill chunks (evictions can add more: the
+    // kernel flags an overflow and the search reruns chained)
+    int64_t ctx_max = 1;
+    for (int64_t i = 0; i < N; ++i) ctx_max = std::max<int64_t>(ctx_max, T->context_len[i]);
+    const int64_t chunks = (cfg->batch_mode == PSG_BATCH_CHUNKED && cfg->chunk_size >= 1)
+                               ? (ctx_max + cfg->chunk_size - 1) / cfg->chunk_size : 1;
+    int64_t per_req = 4 + chunks;
+    if (const char* v = std::getenv("PSG_RLOG_PER_REQ")) per_req = std::max(0, std::atoi(v));  // dev / tests
+    for (int e = 0; e < E; ++e) {  // the replicas of groups >= 1 log
+      const int k0 = entry_unit_begin[e], R = entry_unit_begin[e + 1] - k0, G = entry_groups[e];
+      for (int k = k0 + (G > 1 ? R / G : R); k < k0 + R; ++k) {
+        Unit& u = units[entry_units[k]];
+        u.log_off = rlog_total;
+        u.log_cap = int32_t(std::min<int64_t>(int64_t(u.n_req) * per_req + 64, INT32_MAX));
+        rlog_total += u.log_cap;
+      }
+    }
+  }
+  const int sim_blocks = chain == 1 ? E : chain == 2 ? int(block_k0.size()) : n_units;
 
   std::vector<double> entry_peak(E), entry_freq(E);
   std::vector<int32_t> entry_enc(E);
@@ -935,6 +1005,9 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                o_units = pk.add(units.data(), units.size()),
                o_eub = pk.add(entry_unit_begin.data(), E + 1),
                o_eu = pk.add(entry_units.data(), entry_units.size()),
+               o_bk0 = pk.add(block_k0.data(), block_k0.size()),
+               o_bk1 = pk.add(block_k1.data(), block_k1.size()),
+               o_egr = pk.add(entry_groups.data(), entry_groups.size()),
                o_epeak = pk.add(entry_peak.data(), E), o_eenc = pk.add(entry_enc.data(), E),
                o_efreq = pk.add(entry_freq.data(), E), o_eglob = pk.add(ent.data(), E);
   const size_t o_pmb = cfg->entry_max_batch_size ? pk.add(cfg->entry_max_batch_size, size_t(E)) : 0;
@@ -1023,14 +1096,15 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.anchor = cfg->ttft_anchor;
   sp.memo_cap = 256;
   sp.tab_smem = tab_smem;
-  sp.chain_replicas = 1;
-  if (const char* v = std::getenv("PSG_CHAIN_REPLICAS")) sp.chain_replicas = std::atoi(v) != 0;  // dev knob
+  sp.chain_replicas = chain;
   {
     // The speculation warps pay off while they get SM sub-partitions of their
-    // own: with more than ~1.5 simulation blocks per SM they share them with
-    // other blocks' simulation warps and slow those down (C5: 2 blocks / SM).
-    const int blocks = std::max(sp.chain_replicas ? E : n_units, ctx->concurrent_blocks);
-    sp.speculate = 2 * int64_t(blocks) <= 3 * int64_t(ctx->n_sm) ? 1 : 0;
+    // own: with more than ~2 simulation blocks per SM they share them with
+    // other blocks' simulation warps and slow those down (C5: 437 blocks).
+    const int blocks = std::max(sim_blocks, chain == 2 ? ctx->concurrent_groups : ctx->concurrent_blocks);
+    double per_sm = 2.0;  // (C2 + C2-fp8 bench: 278 group blocks, on; C5: 437, off)
+    if (const char* v = std::getenv("PSG_SPEC_PER_SM")) per_sm = std::atof(v);  // dev knob
+    sp.speculate = double(blocks) <= per_sm * double(ctx->n_sm) ? 1 : 0;
   }
   if (const char* v = std::getenv("PSG_SPECULATE")) sp.speculate = std::atoi(v);  // dev knob: 0 off, 2 idle helper
   sp.spec_sleep_ns = 20;
@@ -1042,7 +1116,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     int64_t max_nr = 0;
     for (const auto& u : units) max_nr = std::max<int64_t>(max_nr, u.n_req);
     const int64_t want = std::max<int64_t>(256, (max_nr + 31) / 32 * 32);
-    const int blocks = std::max(sp.chain_replicas ? E : n_units, ctx->concurrent_blocks);
+    const int blocks = std::max(sim_blocks, chain == 2 ? ctx->concurrent_groups : ctx->concurrent_blocks);
     const int per_sm = std::max(1, (blocks + ctx->n_sm - 1) / std::max(ctx->n_sm, 1));
     const int64_t budget = std::min<int64_t>(ctx->smem_block_max, ctx->smem_sm / per_sm - 1024) -
                            ctx->sim_static_smem;
@@ -1055,6 +1129,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       }
     }
     sp.smem_cap = int(cap);
+    if (const char* v = std::getenv("PSG_SMEM_CAP"))  // dev knob
+      sp.smem_cap = int(std::max<int64_t>(256, std::min<int64_t>(std::atoi(v), cap)) / 32 * 32);
   }
   sp.serial_run = 128;
   if (const char* v = std::getenv("PSG_SERIAL_RUN")) sp.serial_run = std::max(1, std::atoi(v));  // dev knob
@@ -1115,6 +1191,15 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.g_i32 = static_cast<int32_t*>(ctx->d_scratch_i32.p);
   sp.g_f64 = static_cast<double*>(ctx->d_scratch_f64.p);
   sp.g_cm = static_cast<int64_t*>(ctx->d_scratch_cm.p);
+  if (chain == 2) {
+    PSG_CUDA(ctx->d_rlog.ensure(size_t(std::max<int64_t>(rlog_total, 1)) * sizeof(double2)));
+    PSG_CUDA(ctx->d_edone.ensure(size_t(std::max(E, 1)) * sizeof(int32_t)));
+    sp.rlog = static_cast<double2*>(ctx->d_rlog.p);
+    sp.entry_done = static_cast<int32_t*>(ctx->d_edone.p);
+    sp.block_k0 = (const int32_t*)D(o_bk0);
+    sp.block_k1 = (const int32_t*)D(o_bk1);
+    sp.entry_groups = (const int32_t*)D(o_egr);
+  }
 
   ReduceParams rp{};
   rp.n_slots = N;
@@ -1168,7 +1253,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     ++launches;
   }
   if (n_units > 0) {
-    launch_sim(sp.chain_replicas ? E : n_units, smem, st, sp);
+    if (chain == 2) PSG_CUDA(cudaMemsetAsync(sp.entry_done, 0, size_t(E) * sizeof(int32_t), st));
+    launch_sim(sim_blocks, smem, st, sp);
     ++launches;
     PSG_CUDA(cudaGetLastError());
   }
@@ -1200,7 +1286,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       sp.emit_jou = static_cast<double*>(ctx->d_ijou.p);
       sp.emit_off = static_cast<const int64_t*>(ctx->d_ioff.p);
       sp.emit_S = emit_S;
-      launch_sim(sp.chain_replicas ? E : n_units, smem, st, sp);
+      launch_sim(sim_blocks, smem, st, sp);
       ++launches;
       PSG_CUDA(cudaGetLastError());
       // the stepwise pass is a replay: the first pass's outputs are rewritten bit-identically
@@ -1243,6 +1329,13 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       if (eo[e].err && ent[e] < worst) {
         worst = ent[e];
         we = e;
+      }
+    for (int e = 0; e < E; ++e)
+      if (eo[e].err == 9) {  // a replica's tally log overflowed (evictions): rerun chained
+        ctx->chain_fallback = true;
+        const int rc = search_impl(ctx, P, cl, S, T, cfg, out);
+        ctx->chain_fallback = false;
+        return rc;
       }
     if (we >= 0) {
       const int code = eo[we].err;
@@ -1392,14 +1485,26 @@ int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* 
     return PSG_ERR_USAGE;
   // every search's simulation blocks share the device: size shared memory so
   // they are all resident in one wave
-  int total = 0;
+  int total = 0, total_groups = 0;
+  const int groups = replica_groups();
   for (int i = 0; i < n; ++i) {
     if (!ctxs[i] || !plans[i] || !configs[i]) return PSG_ERR_USAGE;
     for (int j = 0; j < i; ++j)
       if (ctxs[j] == ctxs[i]) return PSG_ERR_USAGE;  // one context per search
     const psg_config* c = configs[i];
-    total += c->n_entry_subset > 0 ? c->n_entry_subset
-                                   : plans[i]->n_plans * std::max(1, c->n_freqs);
+    const psg_plan_set* P = plans[i];
+    const int F = std::max(1, c->n_freqs);
+    auto count = [&](int64_t g) {  // global entry g = plan * F + frequency
+      if (g < 0 || g >= int64_t(P->n_plans) * F) return;
+      const int dp = std::max(1, P->model_dp[g / F]);
+      ++total;
+      total_groups += std::min(dp, groups);
+    };
+    if (c->n_entry_subset > 0) {
+      for (int k = 0; k < c->n_entry_subset; ++k) count(c->entry_subset[k]);
+    } else {
+      for (int64_t g = 0; g < int64_t(P->n_plans) * F; ++g) count(g);
+    }
   }
   std::vector<int> rc(size_t(n), PSG_OK);
   StartGate gate;
@@ -1407,12 +1512,14 @@ int psg_search_many(psg_context* const* ctxs, int n, const psg_plan_set* const* 
   const bool gated = !std::getenv("PSG_NO_START_GATE");  // dev knob
   auto run = [&](int i) {
     ctxs[i]->concurrent_blocks = total;
+    ctxs[i]->concurrent_groups = total_groups;
     ctxs[i]->gate = gated ? &gate : nullptr;
     ctxs[i]->gate_passed = false;
     rc[size_t(i)] = psg_search(ctxs[i], plans[i], clusters[i], stores[i], traces[i], configs[i], &outs[i]);
     if (gated && !ctxs[i]->gate_passed) gate.arrive(false);  // failed before the gate
     ctxs[i]->gate = nullptr;
     ctxs[i]->concurrent_blocks = 0;
+    ctxs[i]->concurrent_groups = 0;
   };
   const int spawn = guarded(ctxs[0], [&] {
     std::vector<std::thread> pool;

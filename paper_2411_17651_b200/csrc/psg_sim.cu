@@ -413,7 +413,9 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
 
   // the speculation warp reads the unit's staged state: let it go idle first
-  const bool spec_on = kSpec && !kEmit && p.speculate == 1;  // 2: helper idles (dev)
+  // 2: helper idles (dev); concurrent replicas (chain_replicas == 2) are short
+  // and leave the helper to the DP=1 units
+  const bool spec_on = kSpec && !kEmit && p.speculate == 1;
   if (spec_on)
     while (unsigned(vload(s_spec.done)) != unsigned(vload64(s_spec.job) >> 44)) {
     }
@@ -559,6 +561,15 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const bool missing = p.entry_missing[U.entry] != 0;
 
   double clock = 0.0, energy = 0.0, flops = tally_flops, bytes = tally_bytes;
+  // Replica groups (chain_replicas == 2): the replicas of groups >= 1 log
+  // their tally increments (Unit::log_off >= 0) so the entry's last group to
+  // finish can replay the one running WorkTally (simulator.cpp:195-201) in
+  // replica order.  Records:
+  // {cf, cb} of a mixed iteration, or {-B tag, j} of a j-iteration decode run
+  // at batch B (its increments are the entry's decode-table row).
+  const bool logging = !kEmit && p.chain_replicas == 2 && U.log_off >= 0;
+  double2* const rlog = logging ? p.rlog + U.log_off : nullptr;
+  int nlog = 0;
   int64_t n = 0, max_batch = 0, completed = 0, rejected = 0, sum_batch = 0, admissions = 0;
   int pend = 0, stack_top = 0, w_base = -kWindow;
   // Active slots in admission order with tombstones: B live of len used;
@@ -1095,6 +1106,10 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       energy = __dadd_rn(energy, ce);
       flops = __dadd_rn(flops, cf);
       bytes = __dadd_rn(bytes, cb);
+      if (logging) {
+        if (lane == 0 && nlog < U.log_cap) rlog[nlog] = make_double2(cf, cb);
+        ++nlog;
+      }
       max_batch = max_batch > B ? max_batch : int64_t(B);
       sum_batch += B;
       const int64_t n_new = n + 1;
@@ -1353,6 +1368,12 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       }
       PROF_ADD(6, t_d3);
       n += j;
+      if (logging && j > 0) {
+        if (lane == 0 && nlog < U.log_cap)
+          rlog[nlog] = make_double2(__longlong_as_double(int64_t(B) | INT64_MIN),
+                                    __longlong_as_double(j));
+        ++nlog;
+      }
       used += j * int64_t(B);
       sum_batch += j * int64_t(B);
       if (j > 0) max_batch = max_batch > B ? max_batch : int64_t(B);
@@ -1597,8 +1618,8 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     o.rejected = rejected;
     o.sum_batch = sum_batch;
     o.admissions = admissions;
-    o.err = err;
-    o.pad = 0;
+    o.err = logging && nlog > U.log_cap ? 9 : err;
+    o.nlog = nlog;
     p.uout[unit_idx] = o;
   }
   // clamp flags from the extreme queried token counts / totals: every
@@ -1671,19 +1692,101 @@ __device__ __noinline__ void spec_helper(const unsigned sleep_ns) {
   }
 }
 
+// The entry's WorkTally (simulator.cpp:195-201) from concurrently simulated
+// replica groups (chain_replicas == 2): group 0's chained tally, then every
+// later replica's logged increments in replica order, in the reference's
+// addition order — lane 0 carries flops, lane 1 bytes.  A decode run of j
+// identical additions takes the exact closed form (psg_fastsum.cuh add_n).
+// Runs on the warp of the entry's last group to finish.
+// (Plain pointer arguments: a reference to the kernel's parameter struct
+// would force a local-memory copy of it.)
+__device__ __noinline__ void replay_tally(const int32_t* entry_units, const int kb, const int R,
+                                          const Unit* units, UnitOut* uout, const double2* rlog,
+                                          const double* dt) {
+  const int lane = threadIdx.x & (kWarp - 1);
+  int r1 = 1;  // the first logging replica (group 1)
+  while (r1 < R && units[entry_units[kb + r1]].log_off < 0) ++r1;
+  const UnitOut& o0 = uout[entry_units[kb + r1 - 1]];  // group 0's chained tally
+  double acc = lane == 1 ? __ldcg(&o0.bytes) : __ldcg(&o0.flops);
+  int err = 0;
+  for (int r = r1; r < R && !err; ++r) {
+    const int u = entry_units[kb + r];
+    const int n = __ldcg(&uout[u].nlog);
+    if (n > units[u].log_cap) {
+      err = 9;
+      break;
+    }
+    const double2* rec = rlog + units[u].log_off;
+    for (int base = 0; base < n; base += kWarp) {
+      // a warp of records at a time: lane i loads record base + i (and a
+      // run's increments), then the chains walk them in order
+      const int i = base + lane;
+      double f = 0.0, b = 0.0;
+      long long cnt = 1;
+      if (i < n) {
+        const double2 rc = __ldcg(rec + i);
+        const long long xb = __double_as_longlong(rc.x);
+        if (xb < 0) {  // decode run: {B tag, j}
+          const long long B = xb & 0x7fffffffffffffffll;
+          const double2 fb = __ldg(reinterpret_cast<const double2*>(dt + (B - 1) * 4) + 1);
+          f = fb.x;
+          b = fb.y;
+          cnt = __double_as_longlong(rc.y);
+        } else {
+          f = rc.x;
+          b = rc.y;
+        }
+      }
+      const int m = min(kWarp, n - base);
+      for (int q = 0; q < m; ++q) {
+        const double fi = __shfl_sync(kFull, f, q), bi = __shfl_sync(kFull, b, q);
+        const long long cq = __shfl_sync(kFull, cnt, q);
+        const double inc = lane == 1 ? bi : fi;
+        if (cq <= 8) {
+          for (long long t = 0; t < cq; ++t) acc = __dadd_rn(acc, inc);
+        } else {
+          acc = fastsum::add_n(acc, inc, cq);
+        }
+      }
+    }
+  }
+  UnitOut& ol = uout[entry_units[kb + R - 1]];  // the reduction reads the last replica's tally
+  if (lane == 0) {
+    ol.flops = acc;
+    if (err) ol.err = err;
+  }
+  if (lane == 1) ol.bytes = acc;
+}
+
 // One warp per entry (or unit); with kSpec a second warp per block speculates.
 template <bool kSpec, bool kEmit, int kMode>
 __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
   double tf = 0.0, tb = 0.0;
-  // chained: one warp per entry runs its replicas in order with one running
-  // tally (the reference's WorkTally, so MFU / MBU are bit-exact for DP > 1);
-  // else one warp per unit.  One call site keeps one copy of the loop's code.
+  // chained (1): one warp per entry runs its replicas in order with one
+  // running tally (the reference's WorkTally, so MFU / MBU are bit-exact for
+  // DP > 1); concurrent (2): one warp per unit, the tally replayed below;
+  // 0: one warp per unit.  One call site keeps one copy of the loop's code.
+  const int chain = kEmit ? (p.chain_replicas ? 1 : 0) : p.chain_replicas;
   const int e = blockIdx.x;
-  const int k0 = p.chain_replicas ? p.entry_unit_begin[e] : e;
-  const int k1 = p.chain_replicas ? p.entry_unit_begin[e + 1] : e + 1;
+  const int k0 = chain == 1 ? p.entry_unit_begin[e] : chain == 2 ? p.block_k0[e] : e;
+  const int k1 = chain == 1 ? p.entry_unit_begin[e + 1] : chain == 2 ? p.block_k1[e] : e + 1;
   for (int k = k0; k < k1; ++k) {
-    sim_unit<kSpec, kEmit, kMode>(p, p.chain_replicas ? p.entry_units[k] : k, tf, tb, smem_raw);
+    sim_unit<kSpec, kEmit, kMode>(p, chain == 0 ? k : p.entry_units[k], tf, tb, smem_raw);
     __syncwarp();
+  }
+  const int ent = chain == 2 ? p.units[p.entry_units[k0]].entry : 0;
+  if (chain == 2 && p.entry_groups[ent] > 1) {
+    __threadfence();  // this group's outputs and logs before the count
+    __syncwarp();
+    int last = 0;
+    if ((threadIdx.x & (kWarp - 1)) == 0)
+      last = atomicAdd(p.entry_done + ent, 1) == p.entry_groups[ent] - 1;
+    if (__shfl_sync(kFull, last, 0)) {
+      __threadfence();
+      const int kb = p.entry_unit_begin[ent];
+      replay_tally(p.entry_units, kb, p.entry_unit_begin[ent + 1] - kb, p.units, p.uout, p.rlog,
+                   p.dectab + p.doff[ent] * 4);
+    }
   }
 }
 

@@ -64,20 +64,35 @@ def test_c5_100k_matches_reference(engine, workdir):
     assert len(res) == 301 and res.total_iterations == case.line["plan_iterations"]
 
 
-KERNEL_MODES = [("0", "1"), ("1", "1"), ("0", "0"), ("1", "0")]  # (PSG_SPECULATE, PSG_CHAIN_REPLICAS)
+KERNEL_MODES = [("0", "2"), ("1", "2"), ("0", "1"), ("1", "1"), ("0", "0"),
+                ("1", "0")]  # (PSG_SPECULATE, PSG_CHAIN_REPLICAS)
 
 
 @pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
 @pytest.mark.parametrize("spec,chain", KERNEL_MODES, ids=[f"spec{s}-chain{c}" for s, c in KERNEL_MODES])
 @pytest.mark.parametrize("key", ["c1", "c4"])
 def test_kernel_variants_match_reference(engine, workdir, monkeypatch, key, spec, chain):
-    """Both simulation kernels (with / without the speculation warp) and both
-    replica modes (chained tally / one warp per replica) give the reference's
-    results; unchained, MFU/MBU of DP>1 entries are per-replica partial sums
-    (within 1e-9)."""
+    """Both simulation kernels (with / without the speculation warp) and every
+    replica mode (concurrent replicas with the replayed tally / chained tally /
+    one warp per replica) give the reference's results; unchained (0),
+    MFU/MBU of DP>1 entries are per-replica partial sums (within 1e-9)."""
     monkeypatch.setenv("PSG_SPECULATE", spec)
     monkeypatch.setenv("PSG_CHAIN_REPLICAS", chain)
     case = RefCase(key, workdir)
     res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
-    bad = compare_to_ref(res, case.ref, tally_rtol=0.0 if chain == "1" else 1e-9)
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0 if chain != "0" else 1e-9)
+    assert not bad, "\n".join(bad)
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("key", ["c1", "c2fp8"])
+def test_tally_log_overflow_falls_back(engine, workdir, monkeypatch, key):
+    """Concurrent replicas log their tally increments; a log that outgrows its
+    capacity (forced here: no records per request) makes the search rerun
+    with chained replicas — still bit-exact."""
+    monkeypatch.setenv("PSG_CHAIN_REPLICAS", "2")
+    monkeypatch.setenv("PSG_RLOG_PER_REQ", "0")
+    case = RefCase(key, workdir)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
     assert not bad, "\n".join(bad)
