@@ -3,7 +3,7 @@
 range capture (one bench step between cudaProfilerStart/Stop: every kernel of
 the step, concurrent streams included, in one result):
 
-    PSG_PROFILE_RANGE=1 ncu --replay-mode app-range --profile-from-start off \\
+    PSG_PROFILE_RANGE=1 ncu --replay-mode app-range \\
         --metrics sm__inst_issued.sum,sm__cycles_active.sum,sm__cycles_elapsed.sum,\\
 dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \\
         --csv --log-file gpurun_out/range_<cfg>.csv python bench.py --config <cfg> --steps 1
