@@ -169,7 +169,11 @@ struct EvalOut {
 // curve), lanes 0..3 run the four reference-ordered FP64 chains, then the
 // stage pass.  `item(i)` is the i-th prefill item's token count.  qv / p2p_val
 // are the calling warp's scratch.
-template <typename Item>
+// kPredStages: the stage-energy chain of up to 16 boundaries as predicated
+// straight-line adds (no loop branches; deep pipelines, e.g. C5's pp16).  Only
+// the plain kernel takes it: in the speculation kernel the larger loop costs
+// more than it saves (C2 +2.7%, measured).
+template <bool kPredStages = false, typename Item>
 __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int lane, Item item,
                                                   const int n_items, const int64_t decode,
                                                   const int64_t total, const int64_t* cellq,
@@ -280,7 +284,14 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
     const double j1 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + 1]);
     if (E.NB > 0) cd = dmax_ref(cd, s0);
     if (E.ND == 2) cd = dmax_ref(cd, s1);
-    for (int b = 0; b < E.NB; ++b) ce = __dadd_rn(ce, ((E.p2p_mask >> b) & 1) ? j1 : j0);
+    if (kPredStages && E.NB <= 16) {
+      const unsigned mk = unsigned(E.p2p_mask);
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if (b < E.NB) ce = __dadd_rn(ce, ((mk >> b) & 1u) ? j1 : j0);
+    } else {
+      for (int b = 0; b < E.NB; ++b) ce = __dadd_rn(ce, ((E.p2p_mask >> b) & 1) ? j1 : j0);
+    }
   } else {
     for (int b = 0; b < E.NB; ++b) {
       const int s = __ldg(p2p_slot + b);
@@ -1064,7 +1075,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         __syncwarp();
       } else {
         PROF_T0(t_own);
-        ev = eval_iteration(
+        ev = eval_iteration<!kSpec && !kEmit>(
             ectx, lane, [&](int i) { return a.items[i]; }, n_items, decode, total, cellq, cdesc,
             tab, p2p_slot, qv, p2p_val
 #ifdef PSG_PHASE_PROFILE
