@@ -169,11 +169,13 @@ struct EvalOut {
 // curve), lanes 0..3 run the four reference-ordered FP64 chains, then the
 // stage pass.  `item(i)` is the i-th prefill item's token count.  qv / p2p_val
 // are the calling warp's scratch.
-// kPredStages: the stage-energy chain of up to 16 boundaries as predicated
-// straight-line adds (no loop branches; deep pipelines, e.g. C5's pp16).  Only
-// the plain kernel takes it: in the speculation kernel the larger loop costs
-// more than it saves (C2 +2.7%, measured).
-template <bool kPredStages = false, typename Item>
+// kPlain (the plain kernel, C5's): the knot search on a missed interval hint
+// follows std::upper_bound's probes (log2 steps instead of a scan) and the
+// stage-energy chain of up to 16 boundaries runs as predicated straight-line
+// adds (deep pipelines, e.g. C5's pp16): C5 352 -> 344 ms.  The speculation
+// kernel keeps the compact forms: there the larger code costs more than it
+// saves (C2 +1-3%, measured).
+template <bool kPlain = false, typename Item>
 __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int lane, Item item,
                                                   const int n_items, const int64_t decode,
                                                   const int64_t total, const int64_t* cellq,
@@ -226,7 +228,22 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
       int cnt;
       if (h + 1 < cn && kn[h] <= x && x < kn[h + 1]) {
         cnt = h + 1;
-      } else {
+      } else if (kPlain) {
+        // std::upper_bound's probe sequence (locate, cost.cpp:97): ~log2(cn)
+        // dependent steps instead of a scan of every knot
+        int first = 0, len = cn;
+        while (len > 0) {
+          const int half = len >> 1;
+          if (x < kn[first + half]) {
+            len = half;
+          } else {
+            first += half + 1;
+            len -= half + 1;
+          }
+        }
+        cnt = first;
+        if (cnt >= 1 && cnt < cn) d.hint = cnt - 1;
+      } else {  // (the speculation kernel keeps the compact scan: C2 +1% otherwise)
         cnt = 0;
         for (int j = 0; j < E.n_curve_knots; ++j)
           cnt += (j < cn && kn[j < cn ? j : cn - 1] <= x) ? 1 : 0;
@@ -284,7 +301,7 @@ __device__ __forceinline__ EvalOut eval_iteration(const EvalCtx& E, const int la
     const double j1 = __dadd_rn(o.jrep, p2p_val[kMaxClampSlots + 1]);
     if (E.NB > 0) cd = dmax_ref(cd, s0);
     if (E.ND == 2) cd = dmax_ref(cd, s1);
-    if (kPredStages && E.NB <= 16) {
+    if (kPlain && E.NB > 0 && E.NB <= 16) {
       const unsigned mk = unsigned(E.p2p_mask);
 #pragma unroll
       for (int b = 0; b < 16; ++b)
