@@ -141,6 +141,19 @@ struct SimParams {
   const int32_t* block_k0;   // chain_replicas == 2: block b runs entry_units[block_k0[b] .. block_k1[b])
   const int32_t* block_k1;
   const int32_t* entry_groups;  // chain_replicas == 2: groups of entry e
+  // Streamed results (config.detail): the warp that completes an entry writes
+  // its per-request metrics (id order) and rejected ids straight into the
+  // caller's pinned result arrays at offsets fixed before the launch (the
+  // host derives every entry's completed count from the trace and the KV
+  // budget), so the copy overlaps the entries still simulating.  null: off.
+  psg_request_metrics* out_pr;  // device view of the pinned per_request array
+  int64_t* out_rj;              // ... and of rejected_ids
+  const int64_t* out_pr_off;    // [entries] first record of entry e
+  const int64_t* out_rj_off;
+  const int64_t* out_n_pr;      // [entries] expected completed requests
+  int32_t* out_ok;              // [entries] 1: written (counts matched); else the host compacts
+  const int64_t* slot_id;       // id by slot
+  const int64_t* slot_gen;      // gen_len by slot
 };
 
 // Parameters of the cost-table kernels (psg_tables.cu).

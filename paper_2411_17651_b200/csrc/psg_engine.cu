@@ -162,6 +162,19 @@ struct psg_context {
 
 namespace {
 
+// max{T >= -1 : double(T) * kv <= cap}: the host twin of the simulation's
+// integer KV ledger bound (psg_sim.cu ledger_cap_tokens), same operations.
+int64_t host_cap_tokens(double kv, double cap) {
+  if (!(kv > 0.0)) return (0.0 <= cap) ? (int64_t(1) << 60) : -1;
+  if (!(0.0 <= cap)) return -1;
+  const double q = std::floor(cap / kv);
+  if (q >= 9007199254740992.0) return int64_t(1) << 53;
+  int64_t t = int64_t(q);
+  while (t >= 0 && double(t) * kv > cap) --t;
+  while (!(double(t + 1) * kv > cap)) ++t;
+  return t;
+}
+
 // Replica groups per DP>1 entry (SimParams::chain_replicas 2).
 int replica_groups() {
   if (const char* v = std::getenv("PSG_REPLICA_GROUPS")) return std::max(1, std::atoi(v));  // dev knob
@@ -877,6 +890,37 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   }
   const int sim_blocks = chain == 1 ? E : chain == 2 ? int(block_k0.size()) : n_units;
 
+  // ---- streamed per-request results (SimParams::out_pr) ----
+  // A request completes iff its ledger never has to exceed the KV budget
+  // while it is active: ctx + max(gen - 1, 0) <= cap_tok (admission needs
+  // ctx <= cap_tok, batching.cpp:41-45; an outgrowing request is evicted or,
+  // alone, rejected, :110-125; a request leaves at the step that generates
+  // its last token, before the overflow check).  So every entry's completed
+  // count — and its offset in the result arrays — is known before the
+  // launch, and the warp that completes an entry writes its records straight
+  // into the pinned result arrays while the others still simulate.  The
+  // kernel checks the count; a mismatch falls back to compaction.
+  bool stream = cfg->detail && chain != 0 && !cfg->emit_iterations;
+  if (const char* v = std::getenv("PSG_STREAM_RESULTS")) stream = stream && std::atoi(v) != 0;  // dev knob
+  std::vector<int64_t> exp_pr(stream ? E : 0), pr_off0(stream ? E : 0), rj_off0(stream ? E : 0);
+  int64_t tot_pr0 = 0, tot_rj0 = 0;
+  if (stream) {
+    std::vector<int64_t> need(static_cast<size_t>(N));
+    for (int64_t i = 0; i < N; ++i)
+      need[size_t(i)] = T->context_len[i] + std::max<int64_t>(T->gen_len[i] - 1, 0);
+    std::sort(need.begin(), need.end());
+    for (int e = 0; e < E; ++e) {
+      const int p = int(ent[e] / F);
+      const int64_t ct = host_cap_tokens(P->kv_bytes_per_token[p], P->kv_budget_per_replica[p]);
+      const int64_t c = int64_t(std::upper_bound(need.begin(), need.end(), ct) - need.begin());
+      exp_pr[e] = c;
+      pr_off0[e] = tot_pr0;
+      rj_off0[e] = tot_rj0;
+      tot_pr0 += c;
+      tot_rj0 += N - c;
+    }
+  }
+
   std::vector<double> entry_peak(E), entry_freq(E);
   std::vector<int32_t> entry_enc(E);
   for (int e = 0; e < E; ++e) {
@@ -1008,6 +1052,9 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                o_bk0 = pk.add(block_k0.data(), block_k0.size()),
                o_bk1 = pk.add(block_k1.data(), block_k1.size()),
                o_egr = pk.add(entry_groups.data(), entry_groups.size()),
+               o_xpr = pk.add(exp_pr.data(), exp_pr.size()),
+               o_xpo = pk.add(pr_off0.data(), pr_off0.size()),
+               o_xro = pk.add(rj_off0.data(), rj_off0.size()),
                o_epeak = pk.add(entry_peak.data(), E), o_eenc = pk.add(entry_enc.data(), E),
                o_efreq = pk.add(entry_freq.data(), E), o_eglob = pk.add(ent.data(), E);
   const size_t o_pmb = cfg->entry_max_batch_size ? pk.add(cfg->entry_max_batch_size, size_t(E)) : 0;
@@ -1045,7 +1092,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                w_keys = wk.add<psg_rank_key>(nullptr, E), w_order = wk.add<int64_t>(nullptr, E),
                w_proff = wk.add<int64_t>(nullptr, E), w_rjoff = wk.add<int64_t>(nullptr, E),
                w_tot = wk.add<int64_t>(nullptr, 2), w_cc = wk.add<uint32_t>(nullptr, S->n_compute),
-               w_kc = wk.add<uint32_t>(nullptr, S->n_curves);
+               w_kc = wk.add<uint32_t>(nullptr, S->n_curves),
+               w_ok = wk.add<int32_t>(nullptr, E);
   PSG_CUDA(ctx->d_work.ensure(wk.size + 64));
   PSG_CUDA(ctx->h_out.ensure(wk.size + 64));
 
@@ -1191,6 +1239,25 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.g_i32 = static_cast<int32_t*>(ctx->d_scratch_i32.p);
   sp.g_f64 = static_cast<double*>(ctx->d_scratch_f64.p);
   sp.g_cm = static_cast<int64_t*>(ctx->d_scratch_cm.p);
+  if (stream) {  // the result arrays, pinned and mapped, sized before the launch
+    PSG_CUDA(ctx->h_pr.ensure(std::max<int64_t>(tot_pr0, 1) * sizeof(psg_request_metrics)));
+    PSG_CUDA(ctx->h_rj.ensure(std::max<int64_t>(tot_rj0, 1) * sizeof(int64_t)));
+    void *dpr = nullptr, *drj = nullptr;
+    if (cudaHostGetDevicePointer(&dpr, ctx->h_pr.p, 0) == cudaSuccess &&
+        cudaHostGetDevicePointer(&drj, ctx->h_rj.p, 0) == cudaSuccess) {
+      sp.out_pr = static_cast<psg_request_metrics*>(dpr);
+      sp.out_rj = static_cast<int64_t*>(drj);
+      sp.out_n_pr = (const int64_t*)D(o_xpr);
+      sp.out_pr_off = (const int64_t*)D(o_xpo);
+      sp.out_rj_off = (const int64_t*)D(o_xro);
+      sp.out_ok = (int32_t*)W(w_ok);
+      sp.slot_id = (const int64_t*)D(o_sid);
+      sp.slot_gen = (const int64_t*)D(o_sgen);
+    } else {
+      cudaGetLastError();
+      stream = false;
+    }
+  }
   if (chain == 2) {
     PSG_CUDA(ctx->d_rlog.ensure(size_t(std::max<int64_t>(rlog_total, 1)) * sizeof(double2)));
     PSG_CUDA(ctx->d_edone.ensure(size_t(std::max(E, 1)) * sizeof(int32_t)));
@@ -1349,8 +1416,13 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
 
   // ---- per-request arrays ----
   const int64_t n_pr = cfg->detail ? tot[0] : 0, n_rj = cfg->detail ? tot[1] : 0;
+  bool streamed = stream && n_pr == tot_pr0 && n_rj == tot_rj0;
+  if (streamed) {  // every entry wrote its records during the simulation
+    const auto* okf = reinterpret_cast<const int32_t*>(H(w_ok));
+    for (int e = 0; e < E && streamed; ++e) streamed = okf[e] == 1 && eo[e].completed == exp_pr[e];
+  }
   PSG_CUDA(cudaEventRecord(ctx->ev[5], st));
-  if (cfg->detail) {
+  if (cfg->detail && !streamed) {
     PSG_CUDA(ctx->d_pr.ensure(std::max<int64_t>(n_pr, 1) * sizeof(psg_request_metrics)));
     PSG_CUDA(ctx->d_rj.ensure(std::max<int64_t>(n_rj, 1) * sizeof(int64_t)));
     PSG_CUDA(ctx->h_pr.ensure(std::max<int64_t>(n_pr, 1) * sizeof(psg_request_metrics)));
@@ -1362,7 +1434,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     PSG_CUDA(cudaGetLastError());
   }
   PSG_CUDA(cudaEventRecord(ctx->ev[6], st));
-  if (cfg->detail) {
+  if (cfg->detail && !streamed) {
     if (n_pr)
       PSG_CUDA(cudaMemcpyAsync(ctx->h_pr.p, ctx->d_pr.p, n_pr * sizeof(psg_request_metrics),
                                cudaMemcpyDeviceToHost, st));

@@ -1786,6 +1786,60 @@ __device__ __noinline__ void replay_tally(const int32_t* entry_units, const int 
   if (lane == 1) ol.bytes = acc;
 }
 
+// Streamed results (SimParams::out_pr): entry e's per-request metrics in id
+// order (simulator.cpp:205-206; TPOT's division, :150-152) and its rejected
+// ids (:207), written by the warp that completes the entry into the caller's
+// pinned arrays at the offsets the host fixed.  One pass, four slot groups
+// per step so the loads overlap; writes stay inside the entry's own ranges,
+// and *ok is set only if the entry completed exactly as many requests as
+// the host derived (else the host compacts after the kernels).  Plain
+// pointer arguments (no parameter-struct copy).
+__device__ __noinline__ void stream_entry_results(const uint8_t* st, const double* ttft,
+                                                  const double* tpot_raw, const double* e2e,
+                                                  const int64_t* sid, const int64_t* sgen,
+                                                  const int64_t n, psg_request_metrics* pr,
+                                                  int64_t* rj, const int64_t expect, int32_t* ok) {
+  const int lane = threadIdx.x & (kWarp - 1);
+  const unsigned lt = (1u << lane) - 1u;
+  constexpr int kU = 4;
+  int64_t wc = 0, wr = 0;
+  for (int64_t b = 0; b < n; b += kU * kWarp) {
+    uint8_t v[kU];
+    double t[kU], q[kU], l[kU];
+    int64_t id[kU], g[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {  // issue every load of the step first
+      const int64_t i = b + u * kWarp + lane;
+      v[u] = i < n ? __ldcg(st + i) : 0;
+      const bool c = v[u] == 1;
+      t[u] = c ? __ldcg(ttft + i) : 0.0;
+      q[u] = c ? __ldcg(tpot_raw + i) : 0.0;
+      l[u] = c ? __ldcg(e2e + i) : 0.0;
+      id[u] = v[u] ? sid[i] : 0;
+      g[u] = c ? sgen[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const unsigned cm = __ballot_sync(kFull, v[u] == 1), rm = __ballot_sync(kFull, v[u] == 2);
+      const int64_t pc = wc + __popc(cm & lt), pj = wr + __popc(rm & lt);
+      if (v[u] == 1 && pc < expect) {
+        psg_request_metrics m;
+        m.id = id[u];
+        m.ttft = t[u];
+        m.tpot = g[u] >= 2 ? __ddiv_rn(q[u], double(g[u] - 1)) : 0.0;
+        m.e2e = l[u];
+        m.gen_len = g[u];
+        pr[pc] = m;
+      }
+      if (v[u] == 2 && pj < n - expect) rj[pj] = id[u];
+      wc += __popc(cm);
+      wr += __popc(rm);
+    }
+  }
+  __syncwarp();
+  if (lane == 0 && wc == expect) *ok = 1;
+}
+
 // One warp per entry (or unit); with kSpec a second warp per block speculates.
 template <bool kSpec, bool kEmit, int kMode>
 __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
@@ -1802,19 +1856,28 @@ __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* sme
     sim_unit<kSpec, kEmit, kMode>(p, chain == 0 ? k : p.entry_units[k], tf, tb, smem_raw);
     __syncwarp();
   }
-  const int ent = chain == 2 ? p.units[p.entry_units[k0]].entry : 0;
+  const int ent = chain == 2 ? p.units[p.entry_units[k0]].entry : e;
+  bool last = chain != 0;  // this block completes the entry
   if (chain == 2 && p.entry_groups[ent] > 1) {
     __threadfence();  // this group's outputs and logs before the count
     __syncwarp();
-    int last = 0;
+    int l = 0;
     if ((threadIdx.x & (kWarp - 1)) == 0)
-      last = atomicAdd(p.entry_done + ent, 1) == p.entry_groups[ent] - 1;
-    if (__shfl_sync(kFull, last, 0)) {
+      l = atomicAdd(p.entry_done + ent, 1) == p.entry_groups[ent] - 1;
+    last = __shfl_sync(kFull, l, 0) != 0;
+    if (last) {
       __threadfence();
       const int kb = p.entry_unit_begin[ent];
       replay_tally(p.entry_units, kb, p.entry_unit_begin[ent + 1] - kb, p.units, p.uout, p.rlog,
                    p.dectab + p.doff[ent] * 4);
     }
+  }
+  if (!kEmit && last && p.out_pr) {
+    const size_t base = size_t(ent) * size_t(p.n_slots);
+    stream_entry_results(p.slot_status + base, p.slot_ttft + base, p.slot_tpot + base,
+                         p.slot_e2e + base, p.slot_id, p.slot_gen, p.n_slots,
+                         p.out_pr + p.out_pr_off[ent], p.out_rj + p.out_rj_off[ent],
+                         p.out_n_pr[ent], p.out_ok + ent);
   }
 }
 
