@@ -914,10 +914,11 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       const int64_t ct = host_cap_tokens(P->kv_bytes_per_token[p], P->kv_budget_per_replica[p]);
       const int64_t c = int64_t(std::upper_bound(need.begin(), need.end(), ct) - need.begin());
       exp_pr[e] = c;
+      if (e == 0 && std::getenv("PSG_STREAM_SKEW")) exp_pr[e] += 1;  // dev / tests: force the fallback
       pr_off0[e] = tot_pr0;
       rj_off0[e] = tot_rj0;
-      tot_pr0 += c;
-      tot_rj0 += N - c;
+      tot_pr0 += exp_pr[e];
+      tot_rj0 += N - exp_pr[e];
     }
   }
 

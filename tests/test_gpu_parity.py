@@ -96,3 +96,21 @@ def test_tally_log_overflow_falls_back(engine, workdir, monkeypatch, key):
     res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
     bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
     assert not bad, "\n".join(bad)
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("mode", ["off", "skew"])
+@pytest.mark.parametrize("key", ["c1", "c4"])
+def test_streamed_results_fallback(engine, workdir, monkeypatch, key, mode):
+    """Per-request results are streamed into the pinned result arrays by the
+    warp that completes each entry; with streaming off, or with a completed
+    count that disagrees with the host's derivation (forced), the search
+    falls back to the compaction kernel — bit-exact either way."""
+    if mode == "off":
+        monkeypatch.setenv("PSG_STREAM_RESULTS", "0")
+    else:
+        monkeypatch.setenv("PSG_STREAM_SKEW", "1")
+    case = RefCase(key, workdir)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
+    assert not bad, "\n".join(bad)
