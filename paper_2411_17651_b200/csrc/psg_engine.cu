@@ -602,6 +602,12 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                        psg_result** out) {
   using clk = std::chrono::steady_clock;
   const auto t_start = clk::now();
+  // dev: PSG_HOST_TIMING=1 prints the host phases of the call (ms since entry)
+  static const bool host_timing = std::getenv("PSG_HOST_TIMING") != nullptr;
+  double host_t[16] = {};
+  auto host_mark = [&](int k) {
+    if (host_timing) host_t[k] = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+  };
   if (!ctx || !P || !cl || !S || !T || !cfg || !out) return PSG_ERR_USAGE;
   *out = nullptr;
   ctx->err.clear();
@@ -645,6 +651,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       return fail(ctx, PSG_ERR_USAGE, "plan " + std::to_string(p) + ": p2p boundaries != stages-1");
   }
 
+  host_mark(0);
   // ---- resolve tables (ProfileStore keys, cost.hpp:105-116) ----
   std::map<std::tuple<int, int, long long>, int> cmap;
   for (int t = 0; t < S->n_compute; ++t) {
@@ -728,6 +735,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       }
   }
 
+  host_mark(1);
   // ---- trace canonicalization ----
   const int64_t N = T->n;
   if (N < 0 || N >= INT32_MAX) return fail(ctx, PSG_ERR_USAGE, "trace too large");
@@ -771,6 +779,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                                           std::to_string(slot_id[s]) + " repeats)");
   }
 
+  host_mark(2);
   // ---- units: (entry, replica), longest-first ----
   std::vector<Unit> units;
   std::vector<int32_t> seq;
@@ -890,6 +899,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   }
   const int sim_blocks = chain == 1 ? E : chain == 2 ? int(block_k0.size()) : n_units;
 
+  host_mark(3);
   // ---- streamed per-request results (SimParams::out_pr) ----
   // A request completes iff its ledger never has to exceed the KV budget
   // while it is active: ctx + max(gen - 1, 0) <= cap_tok (admission needs
@@ -933,6 +943,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     entry_enc[e] = P->enc_rank[p];
   }
 
+  host_mark(4);
   // ---- cell signatures and cost-table sizes (psg_tables.cu) ----
   // A cell query depends only on (grid, token_scale, tasks, width, op, op
   // shape) and the token count; plans sharing those share one table.
@@ -1009,6 +1020,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     if (need > tab_smem) gtab_total += (need + 1) & ~int64_t(1);
   }
 
+  host_mark(5);
   // ---- pack inputs ----
   Packer pk;
   const size_t o_model_dp = pk.add(P->model_dp, np), o_stages = pk.add(P->num_stages, np),
@@ -1075,6 +1087,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                o_doff = pk.add(doff.data(), doff.size());
   const size_t in_bytes = pk.size;
 
+  host_mark(6);
   // ---- device buffers ----
   const size_t slots = size_t(E) * size_t(N);
   PSG_CUDA(ctx->d_in.ensure(in_bytes));
@@ -1389,6 +1402,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   const auto* proff = reinterpret_cast<const int64_t*>(H(w_proff));
   const auto* rjoff = reinterpret_cast<const int64_t*>(H(w_rjoff));
 
+  host_mark(7);
   // ---- errors: the lowest global entry index that failed (jobs=1 order) ----
   {
     int64_t worst = INT64_MAX;
@@ -1468,6 +1482,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
       std::fclose(f);
     }
   }
+  host_mark(8);
   // ---- assemble result ----
   ctx->entries.resize(E);
   for (int k = 0; k < E; ++k) {
@@ -1546,6 +1561,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   cudaEventElapsedTime(&b, ctx->ev[6], ctx->ev[7]);
   res->ms_d2h = double(a) + double(b);
   res->ms_total = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+  if (host_timing) {
+    std::fprintf(stderr, "psg host ms: tables %.3f trace %.3f units %.3f stream %.3f sigs %.3f pack %.3f bufs %.3f | errors %.3f assemble %.3f | total %.3f\n",
+                 host_t[0], host_t[1], host_t[2], host_t[3], host_t[4], host_t[5], host_t[6], host_t[7], host_t[8], res->ms_total);
+  }
   *out = res;
   return PSG_OK;
 }
