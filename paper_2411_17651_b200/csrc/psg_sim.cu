@@ -1252,7 +1252,15 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       // iterations until the first finish (inclusive), cut at the first KV
       // overflow (batching.cpp:112): used + k*B > cap_tok
       int64_t kmax = next_fin - n;
-      if (used + kmax * int64_t(B) > cap_tok) kmax = (cap_tok - used) / B + 1;
+      if (used + kmax * int64_t(B) > cap_tok) {
+        // (cap_tok - used) / B + 1 without a 64-bit integer division: both
+        // are < 2^53, so the float quotient is within one of the exact one
+        const int64_t num = cap_tok - used;
+        int64_t q = int64_t(__ddiv_rz(double(num), double(B)));
+        if (q * int64_t(B) > num) --q;
+        if ((q + 1) * int64_t(B) <= num) ++q;
+        kmax = q + 1;
+      }
       // Arrival event: only a not-yet-arrived head can change the batch; an
       // arrived head that admit() left in place stays blocked for the whole
       // run (used only grows, B is fixed).
