@@ -195,3 +195,52 @@ def test_oracle_slo_ranking_partitions_the_reference_order(workdir):
     got = [case.plans.encodings[int(p)] for p in o.entries["plan_index"]]
     assert got == want and list(o.entries["freq_ghz"]) == want_f
     assert 0 < sum(met) < len(met)
+
+
+# ---- the completion rule behind streamed results ------------------------------
+# The engine writes every entry's per-request records into the result arrays
+# during the simulation, at offsets it fixes before the launch from this rule
+# (psg_engine.cu, "streamed per-request results"): a request completes iff
+# ctx + max(gen - 1, 0) fits the plan's KV budget in tokens.  Pinned here on
+# the oracle (itself pinned to the reference) under KV pressure — blocking,
+# LIFO eviction, re-admission, lone rejection, chunked prefill, batch caps.
+
+def cap_tokens(kv, cap):
+    """max{T >= -1 : T * kv <= cap} (psg_sim.cu ledger_cap_tokens)."""
+    if not kv > 0.0:
+        return (1 << 60) if 0.0 <= cap else -1
+    if not 0.0 <= cap:
+        return -1
+    q = math.floor(cap / kv)
+    if q >= 9007199254740992.0:
+        return 1 << 53
+    t = int(q)
+    while t >= 0 and float(t) * kv > cap:
+        t -= 1
+    while not float(t + 1) * kv > cap:
+        t += 1
+    return t
+
+
+def derived_completed(plans_struct, trace_struct, p):
+    ct = cap_tokens(plans_struct.kv_bytes_per_token[p], plans_struct.kv_budget_per_replica[p])
+    return sum(1 for i in range(trace_struct.n)
+               if trace_struct.context_len[i] + max(trace_struct.gen_len[i] - 1, 0) <= ct)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_completion_rule_on_random_batching(seed):
+    for case in (catalog.random_batching(seed), catalog.random_batching_wide(seed)):
+        res = case.oracle()
+        P, T = case.prob.plans.struct, case.prob.trace.struct
+        e = res.entries[0]
+        assert e["num_completed"] == derived_completed(P, T, int(e["plan_index"]))
+
+
+@needs_ref
+@pytest.mark.parametrize("key", ["c1", "c4e"])
+def test_completion_rule_on_config(workdir, key):
+    case = RefCase(key, workdir)
+    for e in case.ref:
+        assert e["num_completed"] == derived_completed(case.plans.struct, case.trace.struct,
+                                                       int(e["plan_index"]))
