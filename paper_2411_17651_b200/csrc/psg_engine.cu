@@ -915,14 +915,24 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   std::vector<int64_t> exp_pr(stream ? E : 0), pr_off0(stream ? E : 0), rj_off0(stream ? E : 0);
   int64_t tot_pr0 = 0, tot_rj0 = 0;
   if (stream) {
-    std::vector<int64_t> need(static_cast<size_t>(N));
-    for (int64_t i = 0; i < N; ++i)
-      need[size_t(i)] = T->context_len[i] + std::max<int64_t>(T->gen_len[i] - 1, 0);
-    std::sort(need.begin(), need.end());
+    // counts of requests with need <= cap for every distinct cap: one pass
+    // over the trace, a binary search among the (few) distinct caps each
+    std::vector<int64_t> caps(static_cast<size_t>(E));
     for (int e = 0; e < E; ++e) {
       const int p = int(ent[e] / F);
-      const int64_t ct = host_cap_tokens(P->kv_bytes_per_token[p], P->kv_budget_per_replica[p]);
-      const int64_t c = int64_t(std::upper_bound(need.begin(), need.end(), ct) - need.begin());
+      caps[size_t(e)] = host_cap_tokens(P->kv_bytes_per_token[p], P->kv_budget_per_replica[p]);
+    }
+    std::vector<int64_t> ucap(caps);
+    std::sort(ucap.begin(), ucap.end());
+    ucap.erase(std::unique(ucap.begin(), ucap.end()), ucap.end());
+    std::vector<int64_t> fit(ucap.size() + 1, 0);  // fit[k]: needs in (ucap[k-1], ucap[k]]
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t need = T->context_len[i] + std::max<int64_t>(T->gen_len[i] - 1, 0);
+      ++fit[size_t(std::lower_bound(ucap.begin(), ucap.end(), need) - ucap.begin())];
+    }
+    for (size_t k = 1; k < fit.size(); ++k) fit[k] += fit[k - 1];  // fit[k]: needs <= ucap[k]
+    for (int e = 0; e < E; ++e) {
+      const int64_t c = fit[size_t(std::lower_bound(ucap.begin(), ucap.end(), caps[size_t(e)]) - ucap.begin())];
       exp_pr[e] = c;
       if (e == 0 && std::getenv("PSG_STREAM_SKEW")) exp_pr[e] += 1;  // dev / tests: force the fallback
       pr_off0[e] = tot_pr0;
