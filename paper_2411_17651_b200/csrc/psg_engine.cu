@@ -765,8 +765,11 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   }
   std::vector<int32_t> slot(N), slot_order(N);
   std::iota(slot_order.begin(), slot_order.end(), 0);
-  std::stable_sort(slot_order.begin(), slot_order.end(),
-                   [&](int32_t a, int32_t b) { return T->id[a] < T->id[b]; });
+  bool ids_sorted = true;  // (the common case: the id order is the trace order)
+  for (int64_t i = 1; i < N && ids_sorted; ++i) ids_sorted = T->id[i - 1] <= T->id[i];
+  if (!ids_sorted)
+    std::stable_sort(slot_order.begin(), slot_order.end(),
+                     [&](int32_t a, int32_t b) { return T->id[a] < T->id[b]; });
   std::vector<int64_t> slot_id(N), slot_gen(N);
   for (int64_t s = 0; s < N; ++s) {
     slot[slot_order[s]] = int32_t(s);
