@@ -80,13 +80,33 @@ def make_case(seed, tight=False):
 
 
 @pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
-@pytest.mark.parametrize("seed,tight", [(s, False) for s in range(24)] + [(s, True) for s in range(100, 116)])
+@pytest.mark.parametrize("seed,tight", [(s, False) for s in range(24)] + [(s, True) for s in range(100, 140)])
 def test_fuzz_search_matches_reference(engine, workdir, seed, tight):
     try:
         case = make_case(seed, tight)
     except Exception as e:  # the planner finds no plan that fits: both sides must agree
         pytest.skip(f"no feasible plan for this random cluster/model: {e}")
     rc, err, ref = case.reference(workdir, f"fuzz{seed}{'t' if tight else ''}")
+    if rc != 0:
+        with pytest.raises(Exception):
+            case.gpu(engine)
+        return
+    same_as_reference(case.gpu(engine), ref)
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("seed", range(100, 112))
+def test_fuzz_tight_small_tally_logs(engine, workdir, monkeypatch, seed):
+    """Memory-tight random problems (evictions, re-admissions) with replica
+    groups whose tally logs hold one record per request: the replicas whose
+    logs overflow make the search rerun chained — bit-exact either way."""
+    monkeypatch.setenv("PSG_CHAIN_REPLICAS", "2")
+    monkeypatch.setenv("PSG_RLOG_PER_REQ", "1")
+    try:
+        case = make_case(seed, True)
+    except Exception as e:
+        pytest.skip(f"no feasible plan for this random cluster/model: {e}")
+    rc, err, ref = case.reference(workdir, f"fuzz{seed}t")
     if rc != 0:
         with pytest.raises(Exception):
             case.gpu(engine)
