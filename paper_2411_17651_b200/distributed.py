@@ -14,16 +14,20 @@ import numpy as np
 from . import abi
 
 
-def entry_costs(problems, freqs_of):
-    """[(estimated cost, problem index, entry index)] — cost = requests per DP
-    replica, the length of the entry's longest serial chain."""
+def entry_costs(problems, freqs_of, groups=2):
+    """[(estimated cost, problem index, entry index)] — cost = the requests of
+    the entry's longest serial chain: a DP=R entry runs as min(R, groups)
+    concurrent replica groups (the engine's default, psg_engine.cu), the
+    largest holding ceil(R / groups) replicas of n / R requests each."""
     out = []
     for pi, prob in enumerate(problems):
         s = prob.plans.struct
         F = max(1, len(freqs_of[pi]))
         n = prob.trace.struct.n
         for e in range(s.n_plans * F):
-            out.append((n / s.model_dp[e // F], pi, e))
+            r = max(1, int(s.model_dp[e // F]))
+            g = max(1, min(r, groups))
+            out.append((n * (-(-r // g)) / r, pi, e))
     return out
 
 
