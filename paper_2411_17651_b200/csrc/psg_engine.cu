@@ -65,7 +65,9 @@ struct HostBuf {
     p = nullptr;
     cap = 0;
     const size_t want = std::max<size_t>(n + n / 4, 4096);
-    cudaError_t e = cudaMallocHost(&p, want);
+    // portable + mapped: the result arrays are written by the kernels of the
+    // context's device directly (streamed results), whatever device is current
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e == cudaSuccess) cap = want;
     return e;
   }
