@@ -65,15 +65,23 @@ def run(key, args):
     res = eng.search(case.plans, case.cluster, case.store, case.trace, case.config())
     raw = np.fromfile(out, dtype=np.uint64).reshape(-1, 2 + len(NAMES))
     meta, cnt = raw[:, :2].view(np.int64), raw[:, 2:]
-    if os.environ.get("PSG_CHAIN_REPLICAS", "1") != "0":
-        # replicas of an entry run in order on one warp: aggregate per entry
-        ents = np.unique(meta[:, 0])
-        agg = np.zeros((len(ents), cnt.shape[1]), dtype=np.uint64)
-        m2 = np.zeros((len(ents), 2), dtype=np.int64)
-        for i, e in enumerate(ents):
-            rows = meta[:, 0] == e
+    chain = os.environ.get("PSG_CHAIN_REPLICAS", "2")
+    groups = int(os.environ.get("PSG_REPLICA_GROUPS", "2")) if chain == "2" else 1
+    if chain != "0":
+        # the replicas of a group run in order on one warp: aggregate per
+        # (entry, group) — replica groups are contiguous replica ranges
+        keys, rows_of = [], {}
+        for u in range(len(meta)):
+            e, r = int(meta[u, 0]), int(meta[u, 1])
+            R = int((meta[:, 0] == e).sum())
+            G = max(1, min(R, groups))
+            g = next(k for k in range(G) if r < (k + 1) * R // G)
+            rows_of.setdefault((e, g), []).append(u)
+        agg = np.zeros((len(rows_of), cnt.shape[1]), dtype=np.uint64)
+        m2 = np.zeros((len(rows_of), 2), dtype=np.int64)
+        for i, ((e, g), rows) in enumerate(sorted(rows_of.items())):
             agg[i] = cnt[rows].sum(axis=0)
-            m2[i] = (e, -int(rows.sum()))  # replica column: -(number of replicas)
+            m2[i] = (e, -len(rows))  # replica column: -(replicas in the group)
         meta, cnt = m2, agg
     order = np.argsort(-cnt[:, 15].astype(np.float64))
     F = max(1, len(case.workload.freqs))
