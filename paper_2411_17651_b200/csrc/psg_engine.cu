@@ -544,6 +544,8 @@ int psg_context_create(int device, psg_context** out) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(ctx->smem_block_max - ctx->sim_static_smem));
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaFuncSetAttribute((const void*)entry_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(kReduceCandCap * kReduceStats * sizeof(uint64_t)));
   *out = ctx;
   return PSG_OK;
 }
@@ -1319,6 +1321,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   rp.ttft_slo = cfg->ttft_slo > 0.0 ? cfg->ttft_slo : 0.0;
   rp.slo_quantile = cfg->slo_quantile > 0.0 ? cfg->slo_quantile : 0.99;
   rp.chain_replicas = sp.chain_replicas;
+  rp.cand_cap = kReduceCandCap;
+  if (const char* v = std::getenv("PSG_REDUCE_CANDIDATES")) rp.cand_cap = std::max(0, std::min(kReduceCandCap, std::atoi(v)));  // dev knob
   sp.entry_unit_begin = rp.entry_unit_begin;
   sp.entry_units = rp.entry_units;
   rp.eout = (EntryOut*)W(w_eout);
@@ -1395,7 +1399,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     }
   }
   PSG_CUDA(cudaEventRecord(ctx->ev[2], st));
-  entry_reduce_kernel<<<E, kReduceThreads, 0, st>>>(rp);
+  entry_reduce_kernel<<<E, kReduceThreads, size_t(rp.cand_cap) * kReduceStats * sizeof(uint64_t), st>>>(rp);
   offsets_kernel<<<1, 32, 0, st>>>(rp.eout, E, (int64_t*)W(w_proff), (int64_t*)W(w_rjoff),
                                    (int64_t*)W(w_tot));
   launches += 2;

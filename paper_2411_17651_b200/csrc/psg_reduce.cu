@@ -38,14 +38,24 @@ __device__ __forceinline__ int64_t nearest_rank(double q, int64_t n) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const ReduceParams r) {
+__global__ void __launch_bounds__(kReduceThreads, 4) entry_reduce_kernel(const ReduceParams r) {
   const int e = blockIdx.x;
-  constexpr int kStats = 6;  // p95 e2e, p50/p99 TTFT, p50/p99 TPOT, TTFT at the SLO quantile
+  constexpr int kStats = kReduceStats;
   __shared__ unsigned sel_hist[kStats][256];
   __shared__ uint64_t sel_prefix[kStats];
   __shared__ int64_t sel_k[kStats];
   __shared__ double sh_sums[2];
-  __shared__ int64_t sh_cnt[2];
+  __shared__ unsigned long long sh_cnt[2];
+  __shared__ double sh_q[kStats];
+  // after four full 8-bit passes, each statistic's remaining candidates (the
+  // keys matching its 24-bit prefix) are gathered here and the four later
+  // passes sweep only them; a statistic with more candidates keeps sweeping
+  // every slot
+  extern __shared__ __align__(16) unsigned char red_smem[];
+  uint64_t* cand = reinterpret_cast<uint64_t*>(red_smem);  // [kStats][cand_cap]
+  __shared__ unsigned cand_n[kStats];
+  const int cand_cap = r.cand_cap;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   const size_t base = size_t(e) * size_t(r.n_slots);
   const uint8_t* st = r.slot_status + base;
@@ -55,63 +65,247 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
   const int64_t* gen = r.slot_gen;  // per slot (id order), shared by entries
 
   // The simulation stores tpot's numerator (finish clock - first token);
-  // the division (simulator.cpp:150-152) runs here, off its serial path.
-  for (int64_t i = threadIdx.x; i < r.n_slots; i += blockDim.x)
-    if (st[i] == 1) tpot[i] = gen[i] >= 2 ? __ddiv_rn(tpot[i], double(gen[i] - 1)) : 0.0;
+  // the division (simulator.cpp:150-152) runs here, off its serial path;
+  // the same sweep counts the completed requests and those with a TPOT.
+  if (threadIdx.x < 2) sh_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < kStats) sh_q[threadIdx.x] = 0.0;
+  __syncthreads();
+  {
+    unsigned lc = 0, lp = 0;
+    for (int64_t i0 = threadIdx.x; i0 < r.n_slots; i0 += kSweepU * blockDim.x) {
+      uint8_t s[kSweepU];
+      int64_t g[kSweepU];
+      double t[kSweepU];
+#pragma unroll
+      for (int u = 0; u < kSweepU; ++u) {  // independent loads first
+        const int64_t i = i0 + int64_t(u) * blockDim.x;
+        const bool in = i < r.n_slots;
+        s[u] = in ? st[i] : 0;
+        g[u] = in ? gen[i] : 0;
+        t[u] = in ? tpot[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kSweepU; ++u)
+        if (s[u] == 1) {
+          const bool g2 = g[u] >= 2;
+          tpot[i0 + int64_t(u) * blockDim.x] = g2 ? __ddiv_rn(t[u], double(g[u] - 1)) : 0.0;
+          ++lc;
+          lp += g2;
+        }
+    }
+    lc = __reduce_add_sync(0xffffffffu, lc);
+    lp = __reduce_add_sync(0xffffffffu, lp);
+    if (lane == 0) {
+      atomicAdd(&sh_cnt[0], (unsigned long long)lc);
+      atomicAdd(&sh_cnt[1], (unsigned long long)lp);
+    }
+  }
+  __syncthreads();
+  const int64_t ncomp = int64_t(sh_cnt[0]), ntpot = int64_t(sh_cnt[1]);
+  const bool slo = r.ttft_slo > 0.0;
+  const bool ext = r.extras != 0, tp = ext && ntpot > 0;
+  const bool act[kStats] = {true, ext, ext, tp, tp, slo};
+  if (ncomp > 0 && threadIdx.x < kStats) {
+    const int j = threadIdx.x;
+    const double q = j == 0 ? 0.95 : (j == 1 || j == 3) ? 0.50 : j == 5 ? r.slo_quantile : 0.99;
+    sel_k[j] = nearest_rank(q, j == 3 || j == 4 ? (ntpot > 0 ? ntpot : 1) : ncomp);
+    sel_prefix[j] = 0;
+  }
   __syncthreads();
 
-  // ---- ordered means: one serial chain in ascending id order ----
-  // The block stages tiles of the slot arrays in shared memory (coalesced),
-  // thread 0 runs the chain from there.  A slot that does not count adds
-  // +0.0, which leaves the non-negative (never -0) sums bit-identical, so the
-  // chain needs no branches.
-  constexpr int kTile = 1024;
-  __shared__ double tile_t[kTile], tile_p[kTile];
-  __shared__ unsigned char tile_c[kTile], tile_g[kTile];
-  double ts = 0.0, ps = 0.0;
-  int64_t pn = 0, cn = 0;
-  for (int64_t b0 = 0; b0 < r.n_slots; b0 += kTile) {
-    const int len = int(min(int64_t(kTile), r.n_slots - b0));
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-      const int64_t q = b0 + i;
-      const bool c = st[q] == 1, g2 = c && gen[q] >= 2;
-      tile_c[i] = c;
-      tile_g[i] = g2;
-      tile_t[i] = c ? ttft[q] : 0.0;
-      tile_p[i] = g2 ? tpot[q] : 0.0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int i = 0;
-      for (; i + 8 <= len; i += 8) {
+  if (warp == 0) {
+    // ---- ordered means (warp 0, beside the order statistics): one serial
+    // chain per mean in ascending id order; the lanes load 128 slots at a
+    // time and broadcast them in order.  A slot that does not count adds
+    // +0.0, which leaves the non-negative (never -0) sums bit-identical. ----
+    constexpr int kU = 4;
+    double ts = 0.0, ps = 0.0;
+    double nt[kU], np[kU];  // the next 128 slots, loaded while the chain runs
+    auto load = [&](int64_t b0) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          ts = __dadd_rn(ts, tile_t[i + u]);
-          ps = __dadd_rn(ps, tile_p[i + u]);
-          cn += tile_c[i + u];
-          pn += tile_g[i + u];
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = b0 + u * 32 + lane;
+        const bool in = i < r.n_slots;
+        const uint8_t s = in ? st[i] : 0;
+        const int64_t g = in ? gen[i] : 0;
+        const double a = in ? ttft[i] : 0.0, b = in ? tpot[i] : 0.0;
+        nt[u] = s == 1 ? a : 0.0;
+        np[u] = s == 1 && g >= 2 ? b : 0.0;
+      }
+    };
+    load(0);
+    for (int64_t b0 = 0; b0 < r.n_slots; b0 += kU * 32) {
+      double vt[kU], vp[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        vt[u] = nt[u];
+        vp[u] = np[u];
+      }
+      if (b0 + kU * 32 < r.n_slots) load(b0 + kU * 32);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          ts = __dadd_rn(ts, __shfl_sync(0xffffffffu, vt[u], q));
+          ps = __dadd_rn(ps, __shfl_sync(0xffffffffu, vp[u], q));
+        }
+    }
+    if (lane == 0) {
+      sh_sums[0] = ts;
+      sh_sums[1] = ps;
+    }
+  } else if (ncomp > 0) {
+    // ---- order statistics (warps 1..): p95 latency (simulator.cpp:222-225),
+    // the p50/p99 TTFT/TPOT extras and the SLO quantile of TTFT, all by one
+    // fused MSB radix select: each 8-bit pass sweeps the slots once and builds
+    // the active statistics' histograms, one warp per statistic picks its
+    // digit.  Named barrier 1 syncs these warps only. ----
+    const int tid = threadIdx.x - 32, nthr = blockDim.x - 32;
+    auto sync_sel = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); };
+    uint64_t mask = 0;
+    bool full[kStats];  // the statistic still sweeps every slot
+    for (int j = 0; j < kStats; ++j) full[j] = true;
+    for (int pass = 7; pass >= 0; --pass) {
+      const int shift = pass * 8;
+      for (int i = tid; i < kStats * 256; i += nthr) sel_hist[i / 256][i % 256] = 0;
+      const bool collect = pass == 4 && cand_cap > 0;  // gather the candidates of the 24-bit prefixes
+      if (collect && tid < kStats) cand_n[tid] = 0;
+      sync_sel();
+      const uint64_t pe = sel_prefix[0], pt50 = sel_prefix[1], pt99 = sel_prefix[2],
+                     pp50 = sel_prefix[3], pp99 = sel_prefix[4], pslo = sel_prefix[5];
+      const bool sweep = full[0] || full[1] || full[2] || full[3] || full[4] || full[5];
+      auto visit = [&](double ve, double vt, double vp, int64_t g) {
+        const uint64_t ke = order_key(ve), m8 = (ke >> shift) & 255u;
+        if (full[0] && (ke & mask) == pe) {
+          atomicAdd(&sel_hist[0][m8], 1u);
+          if (collect) {
+            const unsigned c = atomicAdd(&cand_n[0], 1u);
+            if (c < unsigned(cand_cap)) cand[c] = ke;
+          }
+        }
+        if (ext || slo) {
+          const uint64_t kt = order_key(vt), d = (kt >> shift) & 255u;
+          if (ext && full[1] && (kt & mask) == pt50) {
+            atomicAdd(&sel_hist[1][d], 1u);
+            if (collect) {
+              const unsigned c = atomicAdd(&cand_n[1], 1u);
+              if (c < unsigned(cand_cap)) cand[size_t(cand_cap) + c] = kt;
+            }
+          }
+          if (ext && full[2] && (kt & mask) == pt99) {
+            atomicAdd(&sel_hist[2][d], 1u);
+            if (collect) {
+              const unsigned c = atomicAdd(&cand_n[2], 1u);
+              if (c < unsigned(cand_cap)) cand[2 * size_t(cand_cap) + c] = kt;
+            }
+          }
+          if (slo && full[5] && (kt & mask) == pslo) {
+            atomicAdd(&sel_hist[5][d], 1u);
+            if (collect) {
+              const unsigned c = atomicAdd(&cand_n[5], 1u);
+              if (c < unsigned(cand_cap)) cand[5 * size_t(cand_cap) + c] = kt;
+            }
+          }
+          if (tp && g >= 2) {
+            const uint64_t kp = order_key(vp), dp = (kp >> shift) & 255u;
+            if (full[3] && (kp & mask) == pp50) {
+              atomicAdd(&sel_hist[3][dp], 1u);
+              if (collect) {
+                const unsigned c = atomicAdd(&cand_n[3], 1u);
+                if (c < unsigned(cand_cap)) cand[3 * size_t(cand_cap) + c] = kp;
+              }
+            }
+            if (full[4] && (kp & mask) == pp99) {
+              atomicAdd(&sel_hist[4][dp], 1u);
+              if (collect) {
+                const unsigned c = atomicAdd(&cand_n[4], 1u);
+                if (c < unsigned(cand_cap)) cand[4 * size_t(cand_cap) + c] = kp;
+              }
+            }
+          }
+        }
+      };
+      for (int64_t i0 = tid; sweep && i0 < r.n_slots; i0 += kSweepU * nthr) {
+        uint8_t s[kSweepU];
+        int64_t g[kSweepU];
+        double ve[kSweepU], vt[kSweepU], vp[kSweepU];
+#pragma unroll
+        for (int u = 0; u < kSweepU; ++u) {  // independent loads first
+          const int64_t i = i0 + int64_t(u) * nthr;
+          const bool in = i < r.n_slots;
+          s[u] = in ? st[i] : 0;
+          ve[u] = in ? e2e[i] : 0.0;
+          vt[u] = in && (ext || slo) ? ttft[i] : 0.0;
+          g[u] = in && tp ? gen[i] : 0;
+          vp[u] = in && tp ? tpot[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kSweepU; ++u)
+          if (s[u] == 1) visit(ve[u], vt[u], vp[u], g[u]);
+      }
+      // the statistics swept from their candidates (every key matching the
+      // prefix, so the counts are the full sweep's)
+      for (int j = 0; j < kStats; ++j) {
+        if (full[j] || !act[j]) continue;
+        const uint64_t pj = sel_prefix[j];
+        const uint64_t* cj = cand + size_t(j) * size_t(cand_cap);
+        for (unsigned c = tid; c < cand_n[j]; c += nthr) {
+          const uint64_t k = cj[c];
+          if ((k & mask) == pj) atomicAdd(&sel_hist[j][(k >> shift) & 255u], 1u);
         }
       }
-      for (; i < len; ++i) {
-        ts = __dadd_rn(ts, tile_t[i]);
-        ps = __dadd_rn(ps, tile_p[i]);
-        cn += tile_c[i];
-        pn += tile_g[i];
+      sync_sel();
+      if (collect)  // from the next pass on, statistics whose candidates fit sweep only them
+        for (int j = 0; j < kStats; ++j) full[j] = cand_n[j] > unsigned(cand_cap);
+      const int w = warp - 1;  // warps 1..kStats pick the digits
+      if (w >= 0 && w < kStats && act[w]) {  // first digit whose inclusive count exceeds k (as the serial scan)
+        const int64_t k = sel_k[w];
+        unsigned part = 0;
+        for (int b = 0; b < 8; ++b) part += sel_hist[w][lane * 8 + b];
+        unsigned incl = part;
+        for (int off = 1; off < 32; off <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        const int64_t excl = int64_t(incl - part);
+        const bool here = excl <= k && k < excl + int64_t(part);
+        const unsigned hm = __ballot_sync(0xffffffffu, here);
+        if (hm) {
+          if (lane == __ffs(hm) - 1) {
+            int64_t kk = k - excl;
+            int d = lane * 8;
+            for (; d < lane * 8 + 7; ++d) {
+              if (kk < int64_t(sel_hist[w][d])) break;
+              kk -= sel_hist[w][d];
+            }
+            sel_k[w] = kk;
+            sel_prefix[w] |= uint64_t(d) << shift;
+          }
+        } else if (lane == 31) {  // k beyond every count: digit 255, as the serial scan
+          sel_k[w] = k - (excl + int64_t(part) - int64_t(sel_hist[w][255]));
+          sel_prefix[w] |= uint64_t(255) << shift;
+        }
       }
+      mask |= uint64_t(255) << shift;
+      sync_sel();
     }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    sh_sums[0] = ts;
-    sh_sums[1] = ps;
-    sh_cnt[0] = cn;
-    sh_cnt[1] = pn;
+    if (tid == 0) {
+      sh_q[0] = from_order_key(sel_prefix[0]);
+      if (act[1]) {
+        sh_q[1] = from_order_key(sel_prefix[1]);
+        sh_q[2] = from_order_key(sel_prefix[2]);
+      }
+      if (act[3]) {
+        sh_q[3] = from_order_key(sel_prefix[3]);
+        sh_q[4] = from_order_key(sel_prefix[4]);
+      }
+      if (act[5]) sh_q[5] = from_order_key(sel_prefix[5]);
+    }
   }
   __syncthreads();
-  const int64_t ncomp = sh_cnt[0], ntpot = sh_cnt[1];
 
-  EntryOut o;
   if (threadIdx.x == 0) {
+    EntryOut o;
     o.e2e = 0.0;
     o.energy = 0.0;
     o.flops = 0.0;
@@ -155,96 +349,12 @@ __global__ void __launch_bounds__(kReduceThreads) entry_reduce_kernel(const Redu
                                              double(r.total_devices)));
       }
     }
-  }
-
-  // ---- order statistics: p95 latency (simulator.cpp:222-225), the
-  // p50/p99 TTFT/TPOT extras and the SLO quantile of TTFT, all by one fused
-  // MSB radix select: each 8-bit pass sweeps the slots once and builds the
-  // active statistics' histograms, one warp per statistic picks its digit ----
-  const bool slo = r.ttft_slo > 0.0;
-  double p95 = 0.0, t50 = 0.0, t99 = 0.0, q50 = 0.0, q99 = 0.0, tslo = 0.0;
-  if (ncomp > 0) {
-    const bool ext = r.extras != 0, tp = ext && ntpot > 0;
-    const bool act[kStats] = {true, ext, ext, tp, tp, slo};
-    if (threadIdx.x < kStats) {
-      const int j = threadIdx.x;
-      const double q = j == 0 ? 0.95 : (j == 1 || j == 3) ? 0.50 : j == 5 ? r.slo_quantile : 0.99;
-      sel_k[j] = nearest_rank(q, j == 3 || j == 4 ? (ntpot > 0 ? ntpot : 1) : ncomp);
-      sel_prefix[j] = 0;
-    }
-    uint64_t mask = 0;
-    for (int pass = 7; pass >= 0; --pass) {
-      const int shift = pass * 8;
-      for (int i = threadIdx.x; i < kStats * 256; i += blockDim.x) sel_hist[i / 256][i % 256] = 0;
-      __syncthreads();
-      const uint64_t pe = sel_prefix[0], pt50 = sel_prefix[1], pt99 = sel_prefix[2],
-                     pp50 = sel_prefix[3], pp99 = sel_prefix[4], pslo = sel_prefix[5];
-      for (int64_t i = threadIdx.x; i < r.n_slots; i += blockDim.x) {
-        if (st[i] != 1) continue;
-        const uint64_t ke = order_key(e2e[i]) , m8 = (ke >> shift) & 255u;
-        if ((ke & mask) == pe) atomicAdd(&sel_hist[0][m8], 1u);
-        if (ext || slo) {
-          const uint64_t kt = order_key(ttft[i]), d = (kt >> shift) & 255u;
-          if (ext && (kt & mask) == pt50) atomicAdd(&sel_hist[1][d], 1u);
-          if (ext && (kt & mask) == pt99) atomicAdd(&sel_hist[2][d], 1u);
-          if (slo && (kt & mask) == pslo) atomicAdd(&sel_hist[5][d], 1u);
-          if (tp && gen[i] >= 2) {
-            const uint64_t kp = order_key(tpot[i]), dp = (kp >> shift) & 255u;
-            if ((kp & mask) == pp50) atomicAdd(&sel_hist[3][dp], 1u);
-            if ((kp & mask) == pp99) atomicAdd(&sel_hist[4][dp], 1u);
-          }
-        }
-      }
-      __syncthreads();
-      const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-      if (w < kStats && act[w]) {  // first digit whose inclusive count exceeds k (as the serial scan)
-        const int64_t k = sel_k[w];
-        unsigned part = 0;
-        for (int b = 0; b < 8; ++b) part += sel_hist[w][lane * 8 + b];
-        unsigned incl = part;
-        for (int off = 1; off < 32; off <<= 1) {
-          const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += y;
-        }
-        const int64_t excl = int64_t(incl - part);
-        const bool here = excl <= k && k < excl + int64_t(part);
-        const unsigned hm = __ballot_sync(0xffffffffu, here);
-        if (hm) {
-          if (lane == __ffs(hm) - 1) {
-            int64_t kk = k - excl;
-            int d = lane * 8;
-            for (; d < lane * 8 + 7; ++d) {
-              if (kk < int64_t(sel_hist[w][d])) break;
-              kk -= sel_hist[w][d];
-            }
-            sel_k[w] = kk;
-            sel_prefix[w] |= uint64_t(d) << shift;
-          }
-        } else if (lane == 31) {  // k beyond every count: digit 255, as the serial scan
-          sel_k[w] = k - (excl + int64_t(part) - int64_t(sel_hist[w][255]));
-          sel_prefix[w] |= uint64_t(255) << shift;
-        }
-      }
-      mask |= uint64_t(255) << shift;
-      __syncthreads();
-    }
-    p95 = from_order_key(sel_prefix[0]);
-    if (act[1]) {
-      t50 = from_order_key(sel_prefix[1]);
-      t99 = from_order_key(sel_prefix[2]);
-    }
-    if (act[3]) {
-      q50 = from_order_key(sel_prefix[3]);
-      q99 = from_order_key(sel_prefix[4]);
-    }
-    if (act[5]) tslo = from_order_key(sel_prefix[5]);
-  }
-  if (threadIdx.x == 0) {
-    o.p95 = p95;
-    o.p50_ttft = t50;
-    o.p99_ttft = t99;
-    o.p50_tpot = q50;
-    o.p99_tpot = q99;
+    const double tslo = sh_q[5];
+    o.p95 = sh_q[0];
+    o.p50_ttft = sh_q[1];
+    o.p99_ttft = sh_q[2];
+    o.p50_tpot = sh_q[3];
+    o.p99_tpot = sh_q[4];
     o.slo_ttft = tslo;
     r.eout[e] = o;
     psg_rank_key k;

@@ -18,6 +18,7 @@ struct EntryOut {
 
 struct ReduceParams {
   int64_t n_slots;
+  int32_t cand_cap;          // radix-select candidates per statistic in dynamic shared memory (0: off)
   const uint8_t* slot_status;
   const double *slot_ttft, *slot_e2e;
   double* slot_tpot;  // numerators from the simulation; divided in place by entry_reduce_kernel
@@ -84,9 +85,13 @@ __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per
 __global__ void sim_kernel_emit(const SimParams p);  // iteration-record pass
 __global__ void sim_kernel_chunked(const SimParams p);       // chunked-prefill variants
 __global__ void sim_kernel_spec_chunked(const SimParams p);
-// One CTA per entry; 32 warps hide the slot arrays' load latency in the
-// radix-select sweeps.
-constexpr int kReduceThreads = 1024;
+// One CTA per entry, four resident per SM (a C5 search's 301 entries fit one
+// wave): warp 0 runs the ordered means chain, warps 1..7 the radix select,
+// each thread with kSweepU independent slot loads in flight.
+constexpr int kReduceThreads = 256;
+constexpr int kReduceStats = 6;       // p95 e2e, p50/p99 TTFT, p50/p99 TPOT, TTFT at the SLO quantile
+constexpr int kReduceCandCap = 512;  // radix-select candidates kept per statistic (24 KB)
+constexpr int kSweepU = 4;           // slots per thread per sweep iteration (loads in flight)
 __global__ void entry_reduce_kernel(const ReduceParams r);
 __global__ void offsets_kernel(const EntryOut* eout, int n_entries, int64_t* pr_off,
                                int64_t* rj_off, int64_t* totals);

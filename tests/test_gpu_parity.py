@@ -99,6 +99,20 @@ def test_tally_log_overflow_falls_back(engine, workdir, monkeypatch, key):
 
 
 @pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("cap", ["0", "1", "64"])
+@pytest.mark.parametrize("key", ["c1", "c3"])
+def test_reduce_candidate_paths(engine, workdir, monkeypatch, key, cap):
+    """The radix select's late passes sweep only each statistic's gathered
+    candidates; with no candidate space, or too little for some statistics
+    (they keep sweeping every slot), the quantiles are the same."""
+    monkeypatch.setenv("PSG_REDUCE_CANDIDATES", cap)
+    case = RefCase(key, workdir)
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
+    assert not bad, "\n".join(bad)
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
 @pytest.mark.parametrize("mode", ["off", "skew"])
 @pytest.mark.parametrize("key", ["c1", "c4"])
 def test_streamed_results_fallback(engine, workdir, monkeypatch, key, mode):
