@@ -154,6 +154,14 @@ struct SimParams {
   int32_t* out_ok;              // [entries] 1: written (counts matched); else the host compacts
   const int64_t* slot_id;       // id by slot
   const int64_t* slot_gen;      // gen_len by slot
+  // Mixed-iteration table (psg_tables.cu mixtab_kernel; contiguous batching,
+  // search passes): per tabulated entry, per distinct context length r and
+  // decode count B < mt_w, the whole cost {duration, energy, flops, bytes}
+  // of the iteration {one prefill item of ctx_r tokens, decode = B}.
+  const double* mixtab;         // null: off
+  const int64_t* moff;          // [entries] first row of the entry, or -1
+  const int32_t* t_crank;       // trace index -> rank of its context length
+  int32_t mt_w;                 // decode counts 0 .. mt_w-1 per rank
 };
 
 // Parameters of the cost-table kernels (psg_tables.cu).
@@ -180,6 +188,17 @@ struct TabParams {
   const int32_t* p2p_tab;
   const int32_t* entry_missing;
   double* dectab;
+  // mixed-iteration table (SimParams::mixtab): entries mt_ent[0 .. n_mt)
+  int32_t n_mt;
+  int32_t mt_w;                // decode counts per rank
+  int64_t mt_R;                // distinct context lengths
+  const int32_t* mt_ent;
+  const int64_t* mt_ctx;       // the distinct context lengths, ascending
+  const int64_t* moff;
+  double* mixtab;
+  int64_t mt_T;                // iteration totals 0 .. mt_T-1 of the curve-value table
+  int32_t mt_nq;               // curve slots per total (collectives + <= 2 distinct p2p)
+  double* ctab;                // [n_mt][mt_T][mt_nq] double2
 };
 
 // ---------------------------------------------------------------------------

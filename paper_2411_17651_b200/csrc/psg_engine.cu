@@ -154,7 +154,7 @@ struct psg_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
-  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof;
+  DevBuf d_in, d_slot_f64, d_slot_u8, d_scratch_i32, d_scratch_f64, d_scratch_cm, d_work, d_pr, d_rj, d_qtab, d_dtab, d_prof, d_mtab, d_ctab;
   HostBuf h_in, h_out, h_pr, h_rj, h_it, h_isec, h_ijou;
   DevBuf d_it, d_isec, d_ijou, d_ioff, d_synth, d_plan, d_gtab, d_rlog, d_edone;
   // storage for results handed out (valid until the next call)
@@ -555,7 +555,7 @@ void psg_context_destroy(psg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->d_in, &ctx->d_slot_f64, &ctx->d_slot_u8, &ctx->d_scratch_i32,
-                    &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof,
+                    &ctx->d_scratch_f64, &ctx->d_scratch_cm, &ctx->d_work, &ctx->d_pr, &ctx->d_rj, &ctx->d_qtab, &ctx->d_dtab, &ctx->d_prof, &ctx->d_mtab, &ctx->d_ctab,
                     &ctx->d_it, &ctx->d_isec, &ctx->d_ijou, &ctx->d_ioff, &ctx->d_synth, &ctx->d_plan, &ctx->d_gtab,
                     &ctx->d_rlog, &ctx->d_edone})
     b->release();
@@ -866,6 +866,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   const int groups = replica_groups();
   int64_t rlog_total = 0;
   std::vector<int32_t> block_k0, block_k1, entry_groups(E, 1);
+  std::vector<int64_t> entry_work(E, 0);  // the entry's longest serial chain, in requests
   if (chain == 2) {
     struct Blk { int32_t k0, k1; int64_t work; };
     std::vector<Blk> blks;
@@ -878,6 +879,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
         int64_t w = 0;
         for (int k = a; k < b; ++k) w += units[entry_units[k]].n_req;
         blks.push_back({a, b, w});
+        entry_work[e] = std::max(entry_work[e], w);
       }
     }
     std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.work > y.work; });
@@ -905,6 +907,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     }
   }
   const int sim_blocks = chain == 1 ? E : chain == 2 ? int(block_k0.size()) : n_units;
+  if (chain != 2)
+    for (const auto& u : units)
+      entry_work[u.entry] = chain == 1 ? entry_work[u.entry] + u.n_req
+                                       : std::max<int64_t>(entry_work[u.entry], u.n_req);
 
   host_mark(3);
   // ---- streamed per-request results (SimParams::out_pr) ----
@@ -1024,6 +1030,109 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     ent_plan[e] = int32_t(ent[e] / F);
     ent_fslot[e] = int32_t(ent[e] % F);
   }
+  int speculate;
+  {
+    // The speculation warps pay off while they get SM sub-partitions of their
+    // own: with more than ~2 simulation blocks per SM they share them with
+    // other blocks' simulation warps and slow those down (C5: 437 blocks).
+    const int blocks = std::max(sim_blocks, chain == 2 ? ctx->concurrent_groups : ctx->concurrent_blocks);
+    double per_sm = 2.0;  // (C2 + C2-fp8 bench: 278 group blocks, on; C5: 437, off)
+    if (const char* v = std::getenv("PSG_SPEC_PER_SM")) per_sm = std::atof(v);  // dev knob
+    speculate = double(blocks) <= per_sm * double(ctx->n_sm) ? 1 : 0;
+  }
+  if (const char* v = std::getenv("PSG_SPECULATE")) speculate = std::atoi(v);  // dev knob: 0 off, 2 idle helper
+
+  // ---- mixed-iteration table (psg_tables.cu mixtab_kernel) ----
+  // Under contiguous batching a request is admitted by a mixed iteration
+  // {its whole context, decode = B}.  For the entries whose serial chains
+  // bound the search (longest replica groups), its cost is tabulated per
+  // distinct context length and B < mt_w by a throughput kernel, so their
+  // simulation warps read one row instead of pricing the iteration.
+  std::vector<int64_t> mt_ctx, moff(std::max(E, 1), -1);
+  std::vector<int32_t> t_crank, mt_ent;
+  int mt_w = 256;
+  int64_t mt_bytes = 0, mt_T = 0, ct_bytes = 0;
+  int mt_nq = 1;
+  {
+    int mode = 1;  // 0 off, 1 the entries within mt_frac of the longest chain, 2 every entry
+    if (const char* v = std::getenv("PSG_MIXTAB")) mode = std::atoi(v);  // dev knob
+    double frac = 0.75;
+    if (const char* v = std::getenv("PSG_MIXTAB_FRAC")) frac = std::atof(v);  // dev knob
+    if (const char* v = std::getenv("PSG_MIXTAB_W")) mt_w = std::max(1, std::atoi(v));  // dev knob
+    const int64_t cap_bytes = int64_t(8) << 30;
+    if (mode != 0 && cfg->batch_mode != PSG_BATCH_CHUNKED && !cfg->emit_iterations && E > 0 && N > 0) {
+      int64_t wmax = 0;
+      for (int e = 0; e < E; ++e) wmax = std::max(wmax, entry_work[e]);
+      // curve slots of an entry: its collectives and (at most two, else
+      // not tabulated) distinct p2p curves
+      auto slots_of = [&](int e) {
+        const int p = int(ent[e] / F);
+        std::vector<int32_t> d;
+        for (int b = P->p2p_begin[p]; b < P->p2p_begin[p + 1]; ++b)
+          if (std::find(d.begin(), d.end(), p2p_tab[b]) == d.end()) d.push_back(p2p_tab[b]);
+        return d.size() > 2 ? -1 : P->coll_begin[p + 1] - P->coll_begin[p] + int(d.size());
+      };
+      std::vector<int32_t> sel;
+      for (int e = 0; e < E; ++e)
+        if (!entry_missing[e] && (mode == 2 || double(entry_work[e]) >= frac * double(wmax)) &&
+            slots_of(e) >= 0)
+          sel.push_back(e);
+      if (!sel.empty()) {
+        // distinct context lengths: a dense rank map over [0, max] (one pass
+        // each way) unless the lengths are sparse in a huge range
+        std::vector<int32_t> dense;
+        if (item_max < (int64_t(1) << 22) || item_max < 8 * N) {
+          dense.assign(size_t(item_max) + 1, 0);
+          for (int64_t i = 0; i < N; ++i) dense[size_t(T->context_len[i])] = 1;
+          for (int64_t c = 0; c <= item_max; ++c)
+            if (dense[size_t(c)]) {
+              dense[size_t(c)] = int32_t(mt_ctx.size());
+              mt_ctx.push_back(c);
+            }
+        } else {
+          mt_ctx.assign(T->context_len, T->context_len + N);
+          std::sort(mt_ctx.begin(), mt_ctx.end());
+          mt_ctx.erase(std::unique(mt_ctx.begin(), mt_ctx.end()), mt_ctx.end());
+        }
+        const int64_t R = int64_t(mt_ctx.size());
+        auto need = [&](size_t n) { return R * int64_t(mt_w) * 32 * int64_t(n); };
+        while (need(sel.size()) > cap_bytes && mt_w > 32) mt_w /= 2;
+        if (need(sel.size()) > cap_bytes || sel.size() > 65535) {  // the longest chains first
+          std::stable_sort(sel.begin(), sel.end(),
+                           [&](int32_t a, int32_t b) { return entry_work[a] > entry_work[b]; });
+          sel.resize(std::min<size_t>({sel.size(), size_t(cap_bytes / need(1)), 65535}));
+        }
+        // Worth it when the table costs (measured ~23 ps a row on B200) well
+        // under what it saves the longest chain: ~1,500 cycles (0.76 us) per
+        // mixed iteration priced on the serial path, about one per request —
+        // all of them without speculation, ~30% with it (its misses).
+        const double cost = 23e-12 * double(need(sel.size())) / 32.0;
+        const double gain = 0.76e-6 * double(wmax) * (speculate == 1 ? 0.3 : 1.0);
+        if (mode == 1 && !(cost < 0.5 * gain)) sel.clear();
+        if (!sel.empty()) {
+          t_crank.resize(N);
+          if (!dense.empty()) {
+            for (int64_t i = 0; i < N; ++i) t_crank[i] = dense[size_t(T->context_len[i])];
+          } else {
+            for (int64_t i = 0; i < N; ++i)
+              t_crank[i] = int32_t(std::lower_bound(mt_ctx.begin(), mt_ctx.end(), T->context_len[i]) -
+                                   mt_ctx.begin());
+          }
+          int64_t rows = 0;
+          for (const int32_t e : sel) {
+            moff[e] = rows;
+            rows += R * mt_w;
+          }
+          mt_ent = sel;
+          mt_bytes = rows * 32;
+          for (const int32_t e : sel) mt_nq = std::max(mt_nq, slots_of(e));
+          mt_T = mt_ctx.back() + mt_w;
+          ct_bytes = (int64_t(sel.size()) * mt_T + 1) * mt_nq * 16;  // + one padding row
+        }
+      }
+    }
+  }
+
   // curves staged per unit in shared memory up to 96 KB; a plan with larger
   // curves stages them in the unit's global region instead
   constexpr int64_t kTabSmemCap = 96 * 1024 / int64_t(sizeof(double));
@@ -1102,6 +1211,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
                o_efs = pk.add(ent_fslot.data(), ent_fslot.size()),
                o_erows = pk.add(ent_rows.data(), ent_rows.size()),
                o_doff = pk.add(doff.data(), doff.size());
+  const size_t o_crank = pk.add(t_crank.data(), t_crank.size()),
+               o_mctx = pk.add(mt_ctx.data(), mt_ctx.size()),
+               o_ment = pk.add(mt_ent.data(), mt_ent.size()),
+               o_moff = pk.add(moff.data(), moff.size());
   const size_t in_bytes = pk.size;
 
   host_mark(6);
@@ -1117,6 +1230,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   PSG_CUDA(ctx->d_scratch_cm.ensure((scratch_total / 32 + 2 * int64_t(n_units) + 2) * sizeof(int64_t)));
   PSG_CUDA(ctx->d_qtab.ensure(size_t(std::max<int64_t>(qrows, 1)) * 4 * sizeof(double)));
   PSG_CUDA(ctx->d_dtab.ensure(size_t(std::max<int64_t>(drows, 1)) * 4 * sizeof(double)));
+  if (mt_bytes > 0) {
+    PSG_CUDA(ctx->d_mtab.ensure(size_t(mt_bytes)));
+    PSG_CUDA(ctx->d_ctab.ensure(size_t(ct_bytes)));
+  }
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
   Packer wk;  // offsets only
   const size_t w_uout = wk.add<UnitOut>(nullptr, n_units), w_eout = wk.add<EntryOut>(nullptr, E),
@@ -1176,16 +1293,7 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.memo_cap = 256;
   sp.tab_smem = tab_smem;
   sp.chain_replicas = chain;
-  {
-    // The speculation warps pay off while they get SM sub-partitions of their
-    // own: with more than ~2 simulation blocks per SM they share them with
-    // other blocks' simulation warps and slow those down (C5: 437 blocks).
-    const int blocks = std::max(sim_blocks, chain == 2 ? ctx->concurrent_groups : ctx->concurrent_blocks);
-    double per_sm = 2.0;  // (C2 + C2-fp8 bench: 278 group blocks, on; C5: 437, off)
-    if (const char* v = std::getenv("PSG_SPEC_PER_SM")) per_sm = std::atof(v);  // dev knob
-    sp.speculate = double(blocks) <= per_sm * double(ctx->n_sm) ? 1 : 0;
-  }
-  if (const char* v = std::getenv("PSG_SPECULATE")) sp.speculate = std::atoi(v);  // dev knob: 0 off, 2 idle helper
+  sp.speculate = speculate;
   sp.spec_sleep_ns = 20;
   if (const char* v = std::getenv("PSG_SPEC_SLEEP_NS")) sp.spec_sleep_ns = std::max(0, std::atoi(v));  // dev knob
   {
@@ -1223,6 +1331,10 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   sp.qoff = (const int64_t*)D(o_qoff);
   sp.dectab = static_cast<const double*>(ctx->d_dtab.p);
   sp.doff = (const int64_t*)D(o_doff);
+  sp.mixtab = mt_bytes > 0 ? static_cast<const double*>(ctx->d_mtab.p) : nullptr;
+  sp.moff = (const int64_t*)D(o_moff);
+  sp.t_crank = mt_bytes > 0 ? (const int32_t*)D(o_crank) : nullptr;
+  sp.mt_w = mt_w;
 
   TabParams tp{};
   tp.P = sp.P;
@@ -1250,6 +1362,16 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   tp.p2p_tab = sp.p2p_tab;
   tp.entry_missing = sp.entry_missing;
   tp.dectab = static_cast<double*>(ctx->d_dtab.p);
+  tp.n_mt = int32_t(mt_ent.size());
+  tp.mt_w = mt_w;
+  tp.mt_R = int64_t(mt_ctx.size());
+  tp.mt_ent = (const int32_t*)D(o_ment);
+  tp.mt_ctx = (const int64_t*)D(o_mctx);
+  tp.moff = sp.moff;
+  tp.mixtab = static_cast<double*>(ctx->d_mtab.p);
+  tp.mt_T = mt_T;
+  tp.mt_nq = mt_nq;
+  tp.ctab = static_cast<double*>(ctx->d_ctab.p);
   sp.n_slots = N;
   sp.uout = (UnitOut*)W(w_uout);
   double* slot_f = static_cast<double*>(ctx->d_slot_f64.p);
@@ -1350,6 +1472,13 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   if (E > 0) {
     dectab_kernel<<<dim3(unsigned(E), unsigned(std::min<int64_t>((max_drows + 255) / 256, 65535))),
                     256, 0, st>>>(tp);
+    ++launches;
+  }
+  if (mt_bytes > 0) {  // mixed-iteration rows (read the cell-query and curve-value tables)
+    colltab_kernel<<<dim3(unsigned(tp.n_mt), unsigned(std::min<int64_t>((mt_T + 255) / 256, 65535))),
+                     256, 0, st>>>(tp);
+    mixtab_kernel<<<dim3(unsigned(std::min<int64_t>(tp.mt_R, 65535)), unsigned(tp.n_mt)),
+                    unsigned(std::min(mt_w, 256)), 0, st>>>(tp);
     ++launches;
   }
   if (n_units > 0) {

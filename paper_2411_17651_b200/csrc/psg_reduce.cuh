@@ -103,6 +103,8 @@ __global__ void rank_kernel(const psg_rank_key* keys, int64_t n, int64_t* order)
 size_t sim_smem_bytes(int smem_cap, int memo_cap, int tab_smem, int cm2_cap);
 __global__ void qtab_kernel(const TabParams p);
 __global__ void dectab_kernel(const TabParams p);
+__global__ void mixtab_kernel(const TabParams p);
+__global__ void colltab_kernel(const TabParams p);
 constexpr int kScratchI32 = 7, kScratchF64 = 4;  // per-unit global fallback arrays
 
 }  // namespace psg

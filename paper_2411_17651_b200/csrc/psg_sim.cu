@@ -123,7 +123,7 @@ __shared__ __align__(16) CurveDesc s_cdesc[kMaxClampSlots];       // staged curv
 __shared__ __align__(16) int64_t s_cellq[kMaxCells];              // qtab row 0 per cell
 __shared__ __align__(16) double s_p2p_val[2 * kMaxClampSlots];    // p2p (seconds, joules)
 __shared__ __align__(16) double s_w_arr[kWindow];                 // prefetch window: arrival
-__shared__ __align__(16) int32_t s_w_i32[4 * kWindow];            // tidx, ctx, gen, slot
+__shared__ __align__(16) int32_t s_w_i32[5 * kWindow];            // tidx, ctx, gen, slot, ctx rank
 __shared__ __align__(16) double s_memo[4 * kMemoCap];             // decode-only cost per B
 // closed-form decode runs: per (B, accumulator) the binade segment key
 // (exponent field << 53 | tie << 52 | R; 0 = none), psg_fastsum.cuh segment_key
@@ -376,7 +376,8 @@ __device__ int64_t ledger_cap_tokens(double kv, double cap) {
 // 32 admissions; out of line so the admit path stays compact).
 __device__ __noinline__ void refill_window(const int32_t* seq, const double* arrival,
                                            const int64_t* ctx, const int64_t* gen,
-                                           const int32_t* slot, int64_t seq_base, int replica,
+                                           const int32_t* slot, const int32_t* crank,
+                                           int64_t seq_base, int replica,
                                            int replicas, int n_req, int w_base, bool chunked,
                                            int64_t chunk, int C, const double* qtab,
                                            const int64_t* cellq) {
@@ -389,6 +390,7 @@ __device__ __noinline__ void refill_window(const int32_t* seq, const double* arr
     s_w_i32[kWindow + lane] = int(ctx[t]);
     s_w_i32[2 * kWindow + lane] = int(gen[t]);
     s_w_i32[3 * kWindow + lane] = slot[t];
+    s_w_i32[4 * kWindow + lane] = crank ? crank[t] : -1;
     // warm L1 with the cell rows this request's prefill will read
     int64_t first = ctx[t];
     if (chunked && chunk >= 1 && first > chunk) first = chunk;
@@ -439,6 +441,13 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   const int64_t cap_tok = ledger_cap_tokens(kv, cap);
   const double* qtab = p.qtab;
   const double* dtab = p.dectab + p.doff[U.entry] * 4;  // row B-1 = decode-only cost of B
+  // mixed iterations {one item of a context length, decode B < mt_w}: one
+  // table row (psg_tables.cu mixtab_kernel) instead of pricing them here
+  const double* mtab = nullptr;
+  if (!kEmit && p.mixtab) {
+    const int64_t mo = p.moff[U.entry];
+    if (mo >= 0) mtab = p.mixtab + mo * 4;
+  }
 
   // the speculation warp reads the unit's staged state: let it go idle first
   // 2: helper idles (dev); concurrent replicas (chain_replicas == 2) are short
@@ -606,6 +615,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   int64_t used = 0;  // KV ledger in tokens: sum(ctx + generated) <= cap_tok
   int64_t next_fin = kNoFin;
   int err = 0;
+  int mix_r = -1;  // context-length rank of the last admission (-1: re-admitted from the stack)
   // Lane-resident mode: while the slots fit one warp (the common case), lane i
   // holds slot i in registers and the slot arrays / finish summary are not
   // maintained; spill() switches to the arrays when a 33rd slot is needed and
@@ -651,7 +661,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       PROF_T0(t_ref);
       w_base = pend;
       if (kSpec) {  // out of line: the speculation kernel's admit path stays compact
-        refill_window(p.T.seq, p.T.arrival, p.T.ctx, p.T.gen, p.T.slot, U.seq_base, U.replica,
+        refill_window(p.T.seq, p.T.arrival, p.T.ctx, p.T.gen, p.T.slot, p.t_crank, U.seq_base, U.replica,
                       U.replicas, U.n_req, w_base, chunked, chunk, C, qtab, cellq);
       } else {
         const int j = w_base + lane;
@@ -662,6 +672,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
           w_i32[kWindow + lane] = int(p.T.ctx[t]);
           w_i32[2 * kWindow + lane] = int(p.T.gen[t]);
           w_i32[3 * kWindow + lane] = p.T.slot[t];
+          w_i32[4 * kWindow + lane] = p.t_crank ? p.t_crank[t] : -1;
           // warm L1 with the cell rows this request's prefill will read
           int64_t first = p.T.ctx[t];
           if (chunked && chunk >= 1 && first > chunk) first = chunk;
@@ -977,6 +988,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         ++n_pre;
         ++admissions;
         used += hd_ctx;
+        mix_r = hd_stack ? -1 : w_i32[4 * kWindow + (pend - w_base)];
       } else {
         reject_slot(hd_slot);
       }
@@ -1063,20 +1075,33 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       PROF_T0(t_ev);
       EvalOut ev;
       bool use_spec = false;
-      if (spec_on && n_items == 1 && decode == spec_dec && a.items[0] == spec_tok) {
+      // contiguous batching: a single prefill item is the request admitted in
+      // this pass (every earlier one completed its prefill)
+      const bool use_mt = mtab && n_items == 1 && decode < p.mt_w && mix_r >= 0;
+      if (spec_on && !use_mt && n_items == 1 && decode == spec_dec && a.items[0] == spec_tok) {
         // the speculation warp prices exactly this iteration: wait for it if
         // it has started (it is ahead of us), else price it here
         const unsigned st = unsigned(__shfl_sync(kFull, vload(s_spec.started), 0));
         use_spec = st == spec_seq;
       }
 #ifdef PSG_PHASE_PROFILE
-      if (spec_on && !use_spec) {  // speculation miss: why
+      if (spec_on && !use_spec && !use_mt) {  // speculation miss: why
         const int why = spec_tok < 0 ? 18 : n_items != 1 ? 19 : decode != spec_dec ? 20
                         : a.items[0] != spec_tok ? 21 : 22;
         prof_acc[why] += 1ull;
       }
 #endif
-      if (use_spec) {
+      if (use_mt) {
+        PROF_T0(t_mt);
+        const double2* row = reinterpret_cast<const double2*>(mtab + (int64_t(mix_r) * p.mt_w + decode) * 4);
+        const double2 x = __ldg(row), y = __ldg(row + 1);
+        ev.cd = x.x;
+        ev.ce = x.y;
+        ev.cf = y.x;
+        ev.cb = y.y;
+        ev.srep = ev.jrep = 0.0;
+        PROF_ADD(17, t_mt);
+      } else if (use_spec) {
         PROF_CNT(14);
         PROF_T0(t_wait);
         while (unsigned(vload(s_spec.done)) != spec_seq) {
@@ -1277,7 +1302,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
       // it joins is then exactly this one); the estimate only picks jobs,
       // correctness comes from the exact match at use
       if (spec_on && n_pre == 0 && hd_valid && !hd_stack && hd_arr > clock && !rej_h &&
-          hd_arr < clock + double(next_fin - n) * d) {
+          hd_arr < clock + double(next_fin - n) * d && !(mtab && B < p.mt_w)) {
         int64_t first = hd_ctx;  // the head's first prefill chunk
         if (chunked && first > chunk) first = chunk;
         if ((int(first) != spec_tok || int64_t(B) != spec_dec) && first < (1 << kSpecField) &&

@@ -5,7 +5,7 @@ from paper_2411_17651_b200.host import problem_for
 from paper_2411_17651_b200.inputs import Config
 from paper_2411_17651_b200.workloads import WORKLOADS
 eng = Engine(0)
-ws = [WORKLOADS["c2"], WORKLOADS["c2fp8"]]
+ws = [WORKLOADS[k] for k in (sys.argv[1:] or ["c2", "c2fp8"])]
 probs = [problem_for(w) for w in ws]
 jobs = [(p.plans, p.cluster, p.store, p.trace, Config(objective=w.objective, freqs=w.freqs, detail=True, rank=True)) for p, w in zip(probs, ws)]
 rows = []
