@@ -186,11 +186,16 @@ int replica_groups() {
 void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
   const bool chunked = sp.batch_mode == PSG_BATCH_CHUNKED;
   if (const char* v = std::getenv("PSG_CARVEOUT"))  // dev knob: shared-memory carve-out, percent
-    for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+    for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_lane, (const void*)sim_kernel_emit,
                           (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked})
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(v));
+  // with mixed-iteration tables the table answers the speculation warp's
+  // jobs: the lane-resident kernel without it (C2 -2%)
+  static const bool lane_kernel = !std::getenv("PSG_LANE_KERNEL") || std::atoi(std::getenv("PSG_LANE_KERNEL")) != 0;
   if (sp.emit_it)
     sim_kernel_emit<<<blocks, kWarp, smem, st>>>(sp);
+  else if (sp.speculate == 1 && sp.mixtab && !chunked && lane_kernel)
+    sim_kernel_lane<<<blocks, kWarp, smem, st>>>(sp);
   else if (sp.speculate)
     (chunked ? sim_kernel_spec_chunked : sim_kernel_spec)<<<blocks, 2 * kWarp, smem, st>>>(sp);
   else
@@ -533,13 +538,13 @@ int psg_context_create(int device, psg_context** out) {
   }
   // the cap only; each launch asks for what it needs (set once: contexts may
   // launch concurrently from several threads)
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_lane, (const void*)sim_kernel_emit,
                         (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked}) {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, k) == cudaSuccess)
       ctx->sim_static_smem = std::max<int64_t>(ctx->sim_static_smem, int64_t(fa.sharedSizeBytes));
   }
-  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_emit,
+  for (const void* k : {(const void*)sim_kernel, (const void*)sim_kernel_spec, (const void*)sim_kernel_lane, (const void*)sim_kernel_emit,
                         (const void*)sim_kernel_chunked, (const void*)sim_kernel_spec_chunked})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(ctx->smem_block_max - ctx->sim_static_smem));

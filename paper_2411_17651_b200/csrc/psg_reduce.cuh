@@ -82,6 +82,7 @@ int plan_compute(psg_context* ctx, const psg_plan_space* s, psg_plan_record* rec
                  int32_t* phys, const int64_t* p2p_offset, int32_t* p2p);
 __global__ void sim_kernel(const SimParams p);       // one warp per block
 __global__ void sim_kernel_spec(const SimParams p);  // + a speculation warp per block
+__global__ void sim_kernel_lane(const SimParams p);  // lane-resident slots, no speculation warp
 __global__ void sim_kernel_emit(const SimParams p);  // iteration-record pass
 __global__ void sim_kernel_chunked(const SimParams p);       // chunked-prefill variants
 __global__ void sim_kernel_spec_chunked(const SimParams p);

@@ -402,7 +402,7 @@ __device__ __noinline__ void refill_window(const int32_t* seq, const double* arr
 
 // kMode: batching mode fixed at compile time (1 contiguous, 2 chunked) or
 // read from the parameters (0).
-template <bool kSpec, bool kEmit, int kMode>
+template <bool kSpec, bool kEmit, int kMode, bool kLane = false>
 __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
                                          double& tally_flops, double& tally_bytes,
                                          unsigned char* smem_raw) {
@@ -620,7 +620,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   // holds slot i in registers and the slot arrays / finish summary are not
   // maintained; spill() switches to the arrays when a 33rd slot is needed and
   // fill() switches back once the batch is small again.
-  constexpr bool kReg = kSpec || PSG_REG_ALL;
+  constexpr bool kReg = kSpec || kLane || PSG_REG_ALL;
   bool regm = kReg;
   // Short slot-array mode (!regm, len <= kShortCap): a.fin stays the source
   // of truth, lane l mirrors positions l, 32+l, ... in sf[] so a finish is a
@@ -660,7 +660,7 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
     if (pend >= w_base + kWindow) {  // refill the prefetch window
       PROF_T0(t_ref);
       w_base = pend;
-      if (kSpec) {  // out of line: the speculation kernel's admit path stays compact
+      if (kReg) {  // out of line: the lane-resident kernels' admit path stays compact
         refill_window(p.T.seq, p.T.arrival, p.T.ctx, p.T.gen, p.T.slot, p.t_crank, U.seq_base, U.replica,
                       U.replicas, U.n_req, w_base, chunked, chunk, C, qtab, cellq);
       } else {
@@ -1874,7 +1874,7 @@ __device__ __noinline__ void stream_entry_results(const uint8_t* st, const doubl
 }
 
 // One warp per entry (or unit); with kSpec a second warp per block speculates.
-template <bool kSpec, bool kEmit, int kMode>
+template <bool kSpec, bool kEmit, int kMode, bool kLane = false>
 __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* smem_raw) {
   double tf = 0.0, tb = 0.0;
   // chained (1): one warp per entry runs its replicas in order with one
@@ -1886,7 +1886,7 @@ __device__ __forceinline__ void sim_block(const SimParams& p, unsigned char* sme
   const int k0 = chain == 1 ? p.entry_unit_begin[e] : chain == 2 ? p.block_k0[e] : e;
   const int k1 = chain == 1 ? p.entry_unit_begin[e + 1] : chain == 2 ? p.block_k1[e] : e + 1;
   for (int k = k0; k < k1; ++k) {
-    sim_unit<kSpec, kEmit, kMode>(p, chain == 0 ? k : p.entry_units[k], tf, tb, smem_raw);
+    sim_unit<kSpec, kEmit, kMode, kLane>(p, chain == 0 ? k : p.entry_units[k], tf, tb, smem_raw);
     __syncwarp();
   }
   const int ent = chain == 2 ? p.units[p.entry_units[k0]].entry : e;
@@ -1938,6 +1938,14 @@ __global__ void __launch_bounds__(64, 4) sim_kernel_spec_chunked(const SimParams
 __global__ void __launch_bounds__(32, 8) sim_kernel(const SimParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   sim_block<false, false, 1>(p, smem_raw);
+}
+
+// Lane-resident slots without a speculation warp: contiguous batching with
+// mixed-iteration tables, where the table answers what the speculation warp
+// would have priced.
+__global__ void __launch_bounds__(32, 8) sim_kernel_lane(const SimParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sim_block<false, false, 1, true>(p, smem_raw);
 }
 
 __global__ void __launch_bounds__(32, 8) sim_kernel_chunked(const SimParams p) {
