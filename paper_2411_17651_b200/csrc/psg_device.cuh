@@ -198,7 +198,12 @@ struct TabParams {
   double* mixtab;
   int64_t mt_T;                // iteration totals 0 .. mt_T-1 of the curve-value table
   int32_t mt_nq;               // curve slots per total (collectives + <= 2 distinct p2p)
-  double* ctab;                // [n_mt][mt_T][mt_nq] double2
+  double* ctab;                // [n_mt][mt_nq][mt_T] double2
+  // load test (mixsel_kernel): per tabulated entry the arrival rate of its
+  // longest unit; the mean generation length of the trace
+  const double* mt_lam;
+  double mt_gen;
+  int64_t* moff_rw;            // the same array as moff: -1 drops an entry
 };
 
 // ---------------------------------------------------------------------------

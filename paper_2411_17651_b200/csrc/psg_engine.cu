@@ -1055,6 +1055,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   // simulation warps read one row instead of pricing the iteration.
   std::vector<int64_t> mt_ctx, moff(std::max(E, 1), -1);
   std::vector<int32_t> t_crank, mt_ent;
+  std::vector<double> mt_lam;
+  double mt_gen = 0.0;
   int mt_w = 256;
   int64_t mt_bytes = 0, mt_T = 0, ct_bytes = 0;
   int mt_nq = 1;
@@ -1064,7 +1066,14 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     double frac = 0.75;
     if (const char* v = std::getenv("PSG_MIXTAB_FRAC")) frac = std::atof(v);  // dev knob
     if (const char* v = std::getenv("PSG_MIXTAB_W")) mt_w = std::max(1, std::atoi(v));  // dev knob
-    const int64_t cap_bytes = int64_t(8) << 30;
+    // table memory: at most a quarter of the free device memory (32 GB)
+    int64_t cap_bytes = int64_t(8) << 30;
+    {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+        cap_bytes = std::min<int64_t>(int64_t((free_b + ctx->d_mtab.cap + ctx->d_ctab.cap) / 4),
+                                      int64_t(32) << 30);
+    }
     if (mode != 0 && cfg->batch_mode != PSG_BATCH_CHUNKED && !cfg->emit_iterations && E > 0 && N > 0) {
       int64_t wmax = 0;
       for (int e = 0; e < E; ++e) wmax = std::max(wmax, entry_work[e]);
@@ -1101,7 +1110,6 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
         }
         const int64_t R = int64_t(mt_ctx.size());
         auto need = [&](size_t n) { return R * int64_t(mt_w) * 32 * int64_t(n); };
-        while (need(sel.size()) > cap_bytes && mt_w > 32) mt_w /= 2;
         if (need(sel.size()) > cap_bytes || sel.size() > 65535) {  // the longest chains first
           std::stable_sort(sel.begin(), sel.end(),
                            [&](int32_t a, int32_t b) { return entry_work[a] > entry_work[b]; });
@@ -1130,9 +1138,25 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
           }
           mt_ent = sel;
           mt_bytes = rows * 32;
+          // load test inputs (mixsel_kernel): arrival rate of each entry's
+          // longest unit over the trace's arrival span, mean generation length
+          double a0 = T->arrival[0], a1 = T->arrival[0], g = 0.0;
+          for (int64_t i = 0; i < N; ++i) {
+            a0 = std::min(a0, T->arrival[i]);
+            a1 = std::max(a1, T->arrival[i]);
+            g += double(std::max<int64_t>(T->gen_len[i], 1));
+          }
+          mt_gen = g / double(N);
+          std::vector<int64_t> unit_max(E, 0);
+          for (const auto& u : units) unit_max[u.entry] = std::max<int64_t>(unit_max[u.entry], u.n_req);
+          for (const int32_t e : sel)
+            mt_lam.push_back(a1 > a0 ? double(unit_max[e]) / (a1 - a0) : 0.0);
           for (const int32_t e : sel) mt_nq = std::max(mt_nq, slots_of(e));
           mt_T = mt_ctx.back() + mt_w;
           ct_bytes = (int64_t(sel.size()) * mt_T + 1) * mt_nq * 16;  // + one padding row
+          if (host_timing)
+            std::fprintf(stderr, "psg mixtab: %zu entries x %lld lengths x %d (%.1f MB, est %.2f ms vs %.2f ms)\n",
+                         sel.size(), (long long)R, mt_w, double(mt_bytes) / 1e6, cost * 1e3, gain * 1e3);
         }
       }
     }
@@ -1219,7 +1243,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   const size_t o_crank = pk.add(t_crank.data(), t_crank.size()),
                o_mctx = pk.add(mt_ctx.data(), mt_ctx.size()),
                o_ment = pk.add(mt_ent.data(), mt_ent.size()),
-               o_moff = pk.add(moff.data(), moff.size());
+               o_moff = pk.add(moff.data(), moff.size()),
+               o_mlam = pk.add(mt_lam.data(), mt_lam.size());
   const size_t in_bytes = pk.size;
 
   host_mark(6);
@@ -1377,6 +1402,9 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   tp.mt_T = mt_T;
   tp.mt_nq = mt_nq;
   tp.ctab = static_cast<double*>(ctx->d_ctab.p);
+  tp.mt_lam = (const double*)D(o_mlam);
+  tp.mt_gen = mt_gen;
+  tp.moff_rw = (int64_t*)D(o_moff);
   sp.n_slots = N;
   sp.uout = (UnitOut*)W(w_uout);
   double* slot_f = static_cast<double*>(ctx->d_slot_f64.p);
@@ -1480,6 +1508,11 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     ++launches;
   }
   if (mt_bytes > 0) {  // mixed-iteration rows (read the cell-query and curve-value tables)
+    static const bool mixsel = !std::getenv("PSG_MIXSEL") || std::atoi(std::getenv("PSG_MIXSEL")) != 0;  // dev knob
+    if (mixsel) {
+      mixsel_kernel<<<unsigned((tp.n_mt + 127) / 128), 128, 0, st>>>(tp);
+      ++launches;
+    }
     colltab_kernel<<<dim3(unsigned(tp.n_mt), unsigned(std::min<int64_t>((mt_T + 255) / 256, 65535))),
                      256, 0, st>>>(tp);
     mixtab_kernel<<<dim3(unsigned(std::min<int64_t>(tp.mt_R, 65535)), unsigned(tp.n_mt)),

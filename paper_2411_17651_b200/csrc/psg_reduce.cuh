@@ -106,6 +106,7 @@ __global__ void qtab_kernel(const TabParams p);
 __global__ void dectab_kernel(const TabParams p);
 __global__ void mixtab_kernel(const TabParams p);
 __global__ void colltab_kernel(const TabParams p);
+__global__ void mixsel_kernel(const TabParams p);
 constexpr int kScratchI32 = 7, kScratchF64 = 4;  // per-unit global fallback arrays
 
 }  // namespace psg

@@ -88,6 +88,27 @@ __device__ __forceinline__ void dectab_row(const TabParams& p, const int e, cons
   out[3] = __dmul_rn(__dmul_rn(__dmul_rn(bb, sdd), reps), Sd);
 }
 
+// Load test of the tabulated entries (after dectab_kernel): a table only
+// pays if the entry's batches stay below mt_w.  With decode-only iteration
+// time d(B), a batch of B completes requests at B / (G * d(B)) per second
+// (G: mean generation length); if no B <= 0.8 mt_w keeps up with 1.25x the
+// unit's arrival rate, its queue (and batch) outgrows the table — the entry
+// is dropped (moff = -1): no rows are computed and its simulation prices
+// mixed iterations itself.  Only a cost decision: results do not depend on it.
+__global__ void mixsel_kernel(const TabParams p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n_mt) return;
+  const int e = p.mt_ent[i];
+  const int64_t bt = min(int64_t(0.8 * p.mt_w), p.ent_rows[e]);
+  const double need = 1.25 * p.mt_lam[i];
+  bool ok = false;
+  for (int64_t B = 1; B <= bt && !ok; ++B) {
+    const double d = p.dectab[(p.doff[e] + B - 1) * 4];
+    ok = double(B) >= need * p.mt_gen * d;
+  }
+  if (!ok) p.moff_rw[e] = -1;
+}
+
 // Collective and distinct p2p curve values of a tabulated entry per
 // iteration total T (cost.cpp:262-291): {seconds, joules * groups_per_stage}
 // for collective q < K, {seconds, joules} for the distinct p2p curves (first
@@ -96,6 +117,7 @@ __device__ __forceinline__ void dectab_row(const TabParams& p, const int e, cons
 __global__ void __launch_bounds__(256) colltab_kernel(const TabParams p) {
   const int i = blockIdx.x;
   const int e = p.mt_ent[i], pl = p.ent_plan[e];
+  if (p.moff[e] < 0) return;  // dropped by mixsel_kernel
   const int k0 = p.P.coll_begin[pl], K = p.P.coll_begin[pl + 1] - k0;
   const int b0 = p.P.p2p_begin[pl], b1 = p.P.p2p_begin[pl + 1];
   int d0 = -1, d1 = -1;  // distinct p2p curves
@@ -209,6 +231,7 @@ __global__ void __launch_bounds__(256) mixtab_kernel(const TabParams p) {
   __shared__ double2 s_row[2 * 256];           // the block's rows {duration, energy}, {flops, bytes}
   const int i = blockIdx.y;
   const int e = p.mt_ent[i], pl = p.ent_plan[e], fs = p.ent_fslot[e];
+  if (p.moff[e] < 0) return;  // dropped by mixsel_kernel
   MixEntry m;
   const int c0 = p.P.cell_begin[pl];
   m.C = p.P.cell_begin[pl + 1] - c0;
