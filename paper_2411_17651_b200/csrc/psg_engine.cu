@@ -191,7 +191,8 @@ void launch_sim(int blocks, size_t smem, cudaStream_t st, const SimParams& sp) {
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(v));
   // with mixed-iteration tables the table answers the speculation warp's
   // jobs: the lane-resident kernel without it (C2 -2%)
-  static const bool lane_kernel = !std::getenv("PSG_LANE_KERNEL") || std::atoi(std::getenv("PSG_LANE_KERNEL")) != 0;
+  const char* lk = std::getenv("PSG_LANE_KERNEL");  // dev knob
+  const bool lane_kernel = !lk || std::atoi(lk) != 0;
   if (sp.emit_it)
     sim_kernel_emit<<<blocks, kWarp, smem, st>>>(sp);
   else if (sp.speculate == 1 && sp.mixtab && !chunked && lane_kernel)
@@ -1508,7 +1509,8 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     ++launches;
   }
   if (mt_bytes > 0) {  // mixed-iteration rows (read the cell-query and curve-value tables)
-    static const bool mixsel = !std::getenv("PSG_MIXSEL") || std::atoi(std::getenv("PSG_MIXSEL")) != 0;  // dev knob
+    const char* ms = std::getenv("PSG_MIXSEL");  // dev knob
+    const bool mixsel = !ms || std::atoi(ms) != 0;
     if (mixsel) {
       mixsel_kernel<<<unsigned((tp.n_mt + 127) / 128), 128, 0, st>>>(tp);
       ++launches;

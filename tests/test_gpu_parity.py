@@ -128,3 +128,39 @@ def test_streamed_results_fallback(engine, workdir, monkeypatch, key, mode):
     res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config())
     bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
     assert not bad, "\n".join(bad)
+
+
+# (PSG_MIXTAB, PSG_MIXTAB_W, PSG_MIXSEL, PSG_LANE_KERNEL, PSG_SPECULATE)
+TABLE_MODES = [
+    ("0", "256", "1", "1", ""),    # no table: speculation / own pricing as before
+    ("2", "256", "0", "1", ""),    # every entry tabulated, no load test
+    ("2", "8", "0", "1", ""),      # tiny table: most mixed iterations fall back in-unit
+    ("2", "256", "0", "0", "1"),   # table + speculation warp (spec kernel)
+    ("2", "64", "1", "1", "0"),    # table + plain kernel (no lane-resident slots)
+]
+
+
+@pytest.mark.skipif(not pyoracle.have_refdrv(), reason="oracle/_ref/refdrv not built")
+@pytest.mark.parametrize("mode", TABLE_MODES, ids=["-".join(m) for m in TABLE_MODES])
+@pytest.mark.parametrize("key,extra", [("c1", ()), ("c3", ()), ("c4", ()),
+                                       ("c4", ("--max-batch", "8", "--anchor", "admission"))],
+                         ids=["c1", "c3", "c4", "c4-maxb8"])
+def test_mixed_iteration_tables(engine, workdir, monkeypatch, key, extra, mode):
+    """Mixed iterations read from the per-entry table (psg_tables.cu
+    mixtab_kernel) or priced in the simulation (eval_iteration / the
+    speculation warp), in any mix within one unit and with any kernel
+    variant: the reference's results bit for bit."""
+    mt, w, sel, lane, spec = mode
+    monkeypatch.setenv("PSG_MIXTAB", mt)
+    monkeypatch.setenv("PSG_MIXTAB_W", w)
+    monkeypatch.setenv("PSG_MIXSEL", sel)
+    monkeypatch.setenv("PSG_LANE_KERNEL", lane)
+    if spec:
+        monkeypatch.setenv("PSG_SPECULATE", spec)
+    case = RefCase(key, workdir, extra)
+    kw = {}
+    if "--max-batch" in extra:
+        kw = {"max_batch_size": 8, "ttft_anchor": "admission"}
+    res = engine.search(case.plans, case.cluster, case.store, case.trace, case.config(**kw))
+    bad = compare_to_ref(res, case.ref, tally_rtol=0.0)
+    assert not bad, "\n".join(bad)
