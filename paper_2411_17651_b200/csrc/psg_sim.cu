@@ -616,6 +616,10 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
   int64_t next_fin = kNoFin;
   int err = 0;
   int mix_r = -1;  // context-length rank of the last admission (-1: re-admitted from the stack)
+  // the table row of the mixed iteration the last admission triggers, loaded
+  // at admission (lane l < 4 holds value l) so its latency overlaps the scan
+  double mt_pre = 0.0;
+  int mt_pre_b = -1;  // ... for decode count mt_pre_b
   // Lane-resident mode: while the slots fit one warp (the common case), lane i
   // holds slot i in registers and the slot arrays / finish summary are not
   // maintained; spill() switches to the arrays when a 33rd slot is needed and
@@ -989,6 +993,11 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
         ++admissions;
         used += hd_ctx;
         mix_r = hd_stack ? -1 : w_i32[4 * kWindow + (pend - w_base)];
+        // (slot-array kernel only: the lane-resident loop measured slower with it)
+        if (!kReg && mtab && mix_r >= 0 && B - 1 < p.mt_w) {  // the rest of the batch decodes
+          mt_pre = __ldg(mtab + (int64_t(mix_r) * p.mt_w + (B - 1)) * 4 + (lane & 3));
+          mt_pre_b = B - 1;
+        }
       } else {
         reject_slot(hd_slot);
       }
@@ -1093,12 +1102,19 @@ __device__ __forceinline__ void sim_unit(const SimParams& p, const int unit_idx,
 #endif
       if (use_mt) {
         PROF_T0(t_mt);
-        const double2* row = reinterpret_cast<const double2*>(mtab + (int64_t(mix_r) * p.mt_w + decode) * 4);
-        const double2 x = __ldg(row), y = __ldg(row + 1);
-        ev.cd = x.x;
-        ev.ce = x.y;
-        ev.cf = y.x;
-        ev.cb = y.y;
+        if (!kReg && decode == mt_pre_b) {
+          ev.cd = __shfl_sync(kFull, mt_pre, 0);
+          ev.ce = __shfl_sync(kFull, mt_pre, 1);
+          ev.cf = __shfl_sync(kFull, mt_pre, 2);
+          ev.cb = __shfl_sync(kFull, mt_pre, 3);
+        } else {
+          const double2* row = reinterpret_cast<const double2*>(mtab + (int64_t(mix_r) * p.mt_w + decode) * 4);
+          const double2 x = __ldg(row), y = __ldg(row + 1);
+          ev.cd = x.x;
+          ev.ce = x.y;
+          ev.cf = y.x;
+          ev.cb = y.y;
+        }
         ev.srep = ev.jrep = 0.0;
         PROF_ADD(17, t_mt);
       } else if (use_spec) {
