@@ -151,6 +151,7 @@ struct psg_context {
   int concurrent_groups = 0;       // ... as replica-group blocks (SimParams::chain_replicas 2)
   bool chain_fallback = false;     // rerun with chained replicas (a tally log overflowed)
   int64_t sim_static_smem = 0;     // sim_kernel's static shared memory
+  int64_t mt_cap_bytes = 0;        // mixed-iteration table memory cap (0: not yet queried)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::string err;
@@ -1067,14 +1068,16 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
     double frac = 0.75;
     if (const char* v = std::getenv("PSG_MIXTAB_FRAC")) frac = std::atof(v);  // dev knob
     if (const char* v = std::getenv("PSG_MIXTAB_W")) mt_w = std::max(1, std::atoi(v));  // dev knob
-    // table memory: at most a quarter of the free device memory (32 GB)
-    int64_t cap_bytes = int64_t(8) << 30;
-    {
+    // table memory: at most a quarter of the device memory free when the
+    // context first tabulated (32 GB at most); queried once per context — a
+    // driver query on every call stalls behind other driver clients
+    if (ctx->mt_cap_bytes == 0) {
       size_t free_b = 0, total_b = 0;
-      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-        cap_bytes = std::min<int64_t>(int64_t((free_b + ctx->d_mtab.cap + ctx->d_ctab.cap) / 4),
-                                      int64_t(32) << 30);
+      ctx->mt_cap_bytes = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess
+                              ? std::min<int64_t>(int64_t(free_b / 4), int64_t(32) << 30)
+                              : int64_t(8) << 30;
     }
+    const int64_t cap_bytes = ctx->mt_cap_bytes;
     if (mode != 0 && cfg->batch_mode != PSG_BATCH_CHUNKED && !cfg->emit_iterations && E > 0 && N > 0) {
       int64_t wmax = 0;
       for (int e = 0; e < E; ++e) wmax = std::max(wmax, entry_work[e]);
