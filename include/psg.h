@@ -386,7 +386,11 @@ int psg_plan_emit(psg_context* ctx, const psg_plan_space* space, const psg_plan_
                   psg_plan_soa** out);
 void psg_plan_soa_free(psg_plan_soa* soa);
 
-/* Evaluate-all-plans: plansim::search semantics (see header comment). */
+/* Evaluate-all-plans: plansim::search semantics (see header comment).
+   Device memory grows with the search and stays cached in the context; a
+   contiguous-batching search may add mixed-iteration cost tables for its
+   longest entries, at most a quarter of the free device memory (PSG_MIXTAB=0
+   disables them; results do not depend on them). */
 int psg_search(psg_context* ctx, const psg_plan_set* plans,
                const psg_cluster* cluster, const psg_store* store,
                const psg_trace* trace, const psg_config* config,
