@@ -32,7 +32,12 @@ def deep_case(layers, dp, pp, nodes, n_req=160):
 @needs
 @pytest.mark.parametrize("layers,dp,pp,nodes", [(128, 1, 128, 16), (64, 2, 64, 16), (96, 1, 96, 12)],
                          ids=["pp128", "dp2-pp64", "pp96"])
-def test_deep_pipeline_matches_reference(engine, workdir, layers, dp, pp, nodes):
+@pytest.mark.parametrize("mixtab", ["1", "2"], ids=["auto", "tables"])
+def test_deep_pipeline_matches_reference(engine, workdir, monkeypatch, layers, dp, pp, nodes, mixtab):
+    # tables: every entry gets a mixed-iteration table (stage folds of up to
+    # 127 boundaries over two distinct p2p curves, psg_tables.cu)
+    monkeypatch.setenv("PSG_MIXTAB", mixtab)
+    monkeypatch.setenv("PSG_MIXSEL", "0" if mixtab == "2" else "1")
     case = deep_case(layers, dp, pp, nodes)
     rc, err, ref = case.reference(workdir, f"deep{layers}_{dp}_{pp}")
     assert rc == 0, err
