@@ -1265,8 +1265,15 @@ static int search_impl(psg_context* ctx, const psg_plan_set* P, const psg_cluste
   PSG_CUDA(ctx->d_qtab.ensure(size_t(std::max<int64_t>(qrows, 1)) * 4 * sizeof(double)));
   PSG_CUDA(ctx->d_dtab.ensure(size_t(std::max<int64_t>(drows, 1)) * 4 * sizeof(double)));
   if (mt_bytes > 0) {
-    PSG_CUDA(ctx->d_mtab.ensure(size_t(mt_bytes)));
-    PSG_CUDA(ctx->d_ctab.ensure(size_t(ct_bytes)));
+    // the tables are an optimization: without the memory, search without them
+    if (ctx->d_mtab.ensure(size_t(mt_bytes)) != cudaSuccess ||
+        ctx->d_ctab.ensure(size_t(ct_bytes)) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_mtab.release();
+      ctx->d_ctab.release();
+      std::fill(moff.begin(), moff.end(), int64_t(-1));
+      mt_bytes = ct_bytes = 0;
+    }
   }
   // work: uout, eout, keys, order, pr_off, rj_off, totals, clamp flags
   Packer wk;  // offsets only
