@@ -235,9 +235,9 @@ __global__ void __launch_bounds__(256) mixtab_kernel(const TabParams p) {
   MixEntry m;
   const int c0 = p.P.cell_begin[pl];
   m.C = p.P.cell_begin[pl + 1] - c0;
-  if (int(threadIdx.x) < m.C)
-    s_q[threadIdx.x] = reinterpret_cast<const double2*>(
-        p.qtab + p.qoff[p.cell_sig[size_t(fs) * p.n_cells_total + c0 + threadIdx.x]] * 4);
+  for (int c = threadIdx.x; c < m.C; c += blockDim.x)
+    s_q[c] = reinterpret_cast<const double2*>(
+        p.qtab + p.qoff[p.cell_sig[size_t(fs) * p.n_cells_total + c0 + c]] * 4);
   __syncthreads();
   m.K = p.P.coll_begin[pl + 1] - p.P.coll_begin[pl];
   m.b0 = p.P.p2p_begin[pl];
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) mixtab_kernel(const TabParams p) {
   const int64_t brows = p.ent_rows[e];
   for (int64_t r = blockIdx.x; r < p.mt_R; r += gridDim.x) {
     const int64_t t = p.mt_ctx[r];
-    if (int(threadIdx.x) < 2 * m.C) s_t[threadIdx.x] = __ldg(s_q[threadIdx.x >> 1] + 2 * t + (threadIdx.x & 1));
+    for (int k = threadIdx.x; k < 2 * m.C; k += blockDim.x) s_t[k] = __ldg(s_q[k >> 1] + 2 * t + (k & 1));
     __syncthreads();
     for (int B0 = 0; B0 < p.mt_w; B0 += blockDim.x) {
       const int B = B0 + int(threadIdx.x);

@@ -135,6 +135,7 @@ TABLE_MODES = [
     ("0", "256", "1", "1", ""),    # no table: speculation / own pricing as before
     ("2", "256", "0", "1", ""),    # every entry tabulated, no load test
     ("2", "8", "0", "1", ""),      # tiny table: most mixed iterations fall back in-unit
+    ("2", "3", "0", "1", ""),      # 3-thread table blocks (staging loops narrower than the cells)
     ("2", "256", "0", "0", "1"),   # table + speculation warp (spec kernel)
     ("2", "64", "1", "1", "0"),    # table + plain kernel (no lane-resident slots)
 ]
